@@ -1,0 +1,158 @@
+/*
+ * stkb200.h — C-ABI of the B200 star-stencil backend (libstkb200.so).
+ *
+ * This is the drop-in boundary for the reference's GPU execution path.
+ * Reference interfaces it replaces (paths under the reference package
+ * pkg/src/stencilkit/):
+ *
+ *   - executor.py:491-557  run_tile_plan(unit, GpuPlan, grids) GPU branch, which
+ *     emulates the emitted CUDA in numpy (the Python drop-in sits above this ABI,
+ *     see paper_2309_04671_b200/backend.py::run_gpu);
+ *   - codegen/serial.py:126-208  emit_entry: the only C-ABI the reference has,
+ *     `void run_<target>(T *g0, T *g1, ..., int64_t iter)` over caller-owned,
+ *     padded, C-order host buffers, mutated in place, final contents landed under
+ *     each grid's own name (copy-back, serial.py:191-204);
+ *   - codegen/gpu.py:450-466  _host_stub: the emitted CUDA's host side, which is
+ *     a comment only (no cudaMalloc / memcpy / stream / graph).
+ *
+ * Every entry point returns int (STKB_OK = 0); on failure stkb_last_error()
+ * returns a thread-local message.  Host buffers belong to the caller; device
+ * buffers, streams, CUDA graphs and tensor maps belong to the domain.  Calls on
+ * one domain must be serialised by the caller (one domain per host thread), as
+ * the reference's single-threaded driver does.
+ */
+#ifndef STKB200_H
+#define STKB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STKB_ABI_VERSION 1
+
+/* status codes */
+#define STKB_OK 0
+#define STKB_ERR_ARG 1         /* bad argument (maps to ExecutionError/PlanError) */
+#define STKB_ERR_CUDA 2        /* CUDA runtime/driver failure */
+#define STKB_ERR_UNSUPPORTED 3 /* form/radius/dtype not provided by a tuned kernel */
+#define STKB_ERR_STATE 4       /* call out of order */
+
+/* element types: identical to the STG1 dtype codes, grids.py:13-14 */
+#define STKB_F32 1
+#define STKB_F64 2
+
+/* map kinds */
+#define STKB_MAP_STAR 1 /* dst = (sum_k c_k * src[o_k]) [/ divisor], star offsets, radius <= 4 */
+#define STKB_MAP_WAVE 2 /* dst = a*src[0] + b*prev[0] + vel[0] * (sum_k c_k * src[o_k]) */
+#define STKB_MAP_EXPR 3 /* any kernel: bytecode evaluated in float64, parse order,
+                           one rounding per store (bit-identical to run_target,
+                           executor.py:267-286) */
+
+/* step-program execution precision for STAR/WAVE maps */
+#define STKB_PREC_FAST 0 /* accumulate in the grid dtype with FMA (tolerance-checked) */
+
+/* EXPR bytecode opcodes (5 int32 words per instruction: op, a, b, c, d) */
+#define STKB_OP_CONST 1    /* push consts[a] */
+#define STKB_OP_READ 2     /* push (double) grid_arg[a][p + (b, c, d)] */
+#define STKB_OP_LOCAL 3    /* push locals[a] */
+#define STKB_OP_ADD 4
+#define STKB_OP_SUB 5
+#define STKB_OP_MUL 6
+#define STKB_OP_DIV 7
+#define STKB_OP_NEG 8
+#define STKB_OP_SETLOCAL 9 /* locals[a] = pop */
+#define STKB_OP_STORE 10   /* grid_arg[a][p + (b, c, d)] = (T) pop */
+#define STKB_EXPR_MAX_ARGS 8
+#define STKB_EXPR_MAX_LOCALS 16
+#define STKB_EXPR_MAX_STACK 32
+
+typedef struct stkb_domain stkb_domain;
+
+/* One domain = n_grids named grids sharing dtype, logical shape and halo
+ * order (GridBuffer, grids.py:20-64).  Device layout is pitched: a row of the
+ * contiguous dim d2 starts on a 128-byte boundary and the first interior
+ * element of each row sits at `lead` elements (128 bytes) into the row. */
+typedef struct {
+    int32_t dtype;    /* STKB_F32 | STKB_F64 */
+    int32_t ndim;     /* 3 */
+    int64_t shape[3]; /* interior extents (d0 streaming/slab axis, d1, d2 contiguous) */
+    int32_t order;    /* halo width on every side, >= every kernel radius */
+    int32_t n_grids;  /* number of named grids (names are 0..n_grids-1) */
+    int32_t device;   /* CUDA device ordinal */
+    int32_t flags;    /* reserved, 0 */
+} stkb_domain_desc;
+
+typedef struct {
+    int32_t kind;      /* STKB_MAP_* */
+    int32_t radius;    /* STAR/WAVE: star radius 1..4 */
+    int32_t src;       /* STAR/WAVE: name read at the star offsets */
+    int32_t dst;       /* STAR/WAVE: name written at offset 0 */
+    int32_t prev;      /* WAVE: name read at offset 0 (may equal dst: in-place) */
+    int32_t vel;       /* WAVE: name read at offset 0 (velocity / kappa) */
+    int32_t precision; /* STKB_PREC_FAST */
+    int32_t tag;       /* caller's map id, reported by stkb_nonfinite */
+    /* STAR/WAVE coefficients: coef[0] = centre; axis a (0=d0,1=d1,2=d2), distance
+     * m in 1..radius: coef[1 + a*2*radius + 2*(m-1) + 0] for offset -m,
+     *                 coef[1 + a*2*radius + 2*(m-1) + 1] for offset +m. */
+    double coef[25];
+    double divisor; /* STAR: 0 = none, else the sum is divided by it */
+    double wave_a;  /* WAVE */
+    double wave_b;  /* WAVE */
+    int64_t lo[3];  /* output region box, interior coordinates, half open */
+    int64_t hi[3];
+    /* EXPR only */
+    int32_t n_args;                        /* kernel grid params */
+    int32_t args[STKB_EXPR_MAX_ARGS];      /* name bound to each grid param */
+    int32_t n_code;                        /* instructions (5 words each) */
+    const int32_t *code;
+    int32_t n_consts;
+    const double *consts;
+} stkb_map_desc;
+
+/* library */
+int stkb_abi_version(void);
+const char *stkb_last_error(void);
+int stkb_device_count(int32_t *count);
+
+/* domain lifetime and layout */
+int stkb_domain_create(const stkb_domain_desc *desc, stkb_domain **out);
+int stkb_domain_destroy(stkb_domain *dom);
+int stkb_layout(const stkb_domain *dom, int64_t *pitch_elems, int64_t *plane_elems,
+                int64_t *lead_elems, int64_t *buffer_elems);
+int stkb_device_ptr(stkb_domain *dom, int32_t name, void **dptr);
+int stkb_set_stream(stkb_domain *dom, void *cuda_stream); /* NULL = domain's own */
+
+/* host <-> device, GridBuffer.data layout (C-order, padded, unpitched) */
+int stkb_upload(stkb_domain *dom, int32_t name, const void *host_padded);
+int stkb_download(stkb_domain *dom, int32_t name, void *host_padded);
+int stkb_upload_async(stkb_domain *dom, int32_t name, const void *host_padded);
+int stkb_download_async(stkb_domain *dom, int32_t name, void *host_padded);
+
+/* step program: a sequence of maps and swaps replayed `steps` times */
+int stkb_program_reset(stkb_domain *dom);
+int stkb_program_add_map(stkb_domain *dom, const stkb_map_desc *map);
+int stkb_program_add_swap(stkb_domain *dom, int32_t a, int32_t b);
+int stkb_run(stkb_domain *dom, int64_t steps); /* CUDA-graph replay, async */
+int stkb_run_once(stkb_domain *dom);             /* one step, direct launches (ncu-friendly) */
+int stkb_sync(stkb_domain *dom);
+int stkb_elapsed_ms(stkb_domain *dom, double *ms); /* device time of the last stkb_run */
+int stkb_launches(stkb_domain *dom, int64_t *count); /* kernels launched by the last stkb_run */
+int stkb_binding(const stkb_domain *dom, int32_t name, int32_t *buffer);
+int stkb_nonfinite(stkb_domain *dom, int32_t tag, int32_t *flag); /* sticky; clears it */
+
+/* Compatibility entry with the reference C-ABI's semantics (serial.py:126-208):
+ * upload every grid, run the program `iters` times, download every grid under
+ * its final name, synchronously.  host[i] is GridBuffer.data of name i. */
+int stkb_run_target(stkb_domain *dom, void *const *host, int64_t iters);
+
+/* device-side comparison (grids.py:163-174): max |a-b|, sum (a-b)^2, argmax,
+ * max |a| over the interior of two names (a is the reference side). */
+int stkb_compare(stkb_domain *dom, int32_t a, int32_t b, double *max_err, double *sum_sq,
+                 int64_t *worst_flat, double *scale);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STKB200_H */

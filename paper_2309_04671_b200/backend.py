@@ -1,0 +1,332 @@
+"""Drop-in GPU execution of bound stencil targets on B200.
+
+:func:`run_gpu` has exactly the signature and contract of the reference's
+``run_tile_plan`` (executor.py:491-557) for a ``GpuPlan``: it copies its
+inputs, honours ``BoundSwap`` name semantics, walks ``BoundFor`` loops
+(runtime bounds from ``bindings``), warns on non-finite results
+(executor.py:247-253) and returns a new ``{name: GridBuffer}`` dict.  Instead
+of emulating the emitted CUDA in numpy it uploads the grids once into
+pitched HBM buffers, replays the loop body on the device as a CUDA graph and
+downloads once.  There is no CPU fallback: without the CUDA library or a GPU
+it raises.
+
+:class:`DeviceTarget` is the same machinery kept resident, for repeated runs
+and for timing (bench.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import warnings
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+from .matcher import MapPlan, MatchError, match_map
+from .program import stmt_kind
+
+GPU_TEMPLATES = ("gmem", "smem", "f4", "shift", "unroll", "semi")
+
+
+class ExecutionError(ValueError):
+    """Mirror of executor.py:34-35 (a ValueError, exit code 1 in the CLI)."""
+
+
+def _prepare(unit, target, args, scheme):
+    if hasattr(unit, "stmts") and hasattr(unit, "grid_params"):
+        return unit
+    try:  # a reference SourceUnit: bind it with the reference front end
+        from stencilkit.analysis import bind_target  # type: ignore
+    except ImportError:
+        raise ExecutionError("run_gpu needs a BoundTarget (the stencilkit front end is not importable)") from None
+    return bind_target(unit, target, args, scheme)
+
+
+def _maps(stmts):
+    for s in stmts:
+        k = stmt_kind(s)
+        if k == "BoundMap":
+            yield s
+        elif k == "BoundFor":
+            yield from _maps(s.body)
+
+
+def check_plan(plan, bound) -> None:
+    """The GPU-branch plan checks of run_tile_plan (executor.py:529-543)."""
+    template = getattr(plan, "template", None)
+    if template not in GPU_TEMPLATES or not hasattr(plan, "dims"):
+        raise ExecutionError(f"cannot execute plan {plan!r} on the GPU backend")
+    for bmap in _maps(bound.stmts):
+        dims = bmap.info.dims
+        if plan.dims != dims:
+            raise ExecutionError(f"plan is {plan.dims}D but kernel '{bmap.kernel.name}' is {dims}D")
+        if template == "semi" and bmap.info.shape != "star":
+            raise ExecutionError("semi execution supports star-shaped stencils only")
+        if template in ("shift", "unroll", "semi") and dims < 2:
+            raise ExecutionError("streaming templates need a 2D or 3D kernel")
+
+
+def default_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class DeviceTarget:
+    """The grids of one bound target resident in HBM, plus its compiled maps."""
+
+    def __init__(self, grids: dict, names: Optional[list] = None, device: Optional[int] = None,
+                 precision: str = "fast"):
+        if precision not in ("fast", "exact"):
+            raise ExecutionError(f"unknown precision '{precision}' (fast | exact)")
+        self.precision = precision
+        self.lib = L.load()
+        self.names = list(names if names is not None else grids)
+        if not self.names:
+            raise ExecutionError("no grids to place on the device")
+        ref = grids[self.names[0]]
+        for n in self.names:
+            g = grids[n]
+            if (g.dtype, tuple(g.shape), g.order) != (ref.dtype, tuple(ref.shape), ref.order):
+                raise ExecutionError(
+                    f"grid '{n}' is {g.dtype}{tuple(g.shape)}/order {g.order}; the device domain needs every "
+                    f"grid of a target to match {ref.dtype}{tuple(ref.shape)}/order {ref.order}")
+        if ref.dtype not in ("f32", "f64"):
+            raise ExecutionError(f"unsupported dtype {ref.dtype}")
+        nd = len(ref.shape)
+        if nd not in (2, 3):
+            raise ExecutionError(f"{nd}-D grids are not supported on the device")
+        self.dtype, self.shape, self.order = ref.dtype, tuple(ref.shape), ref.order
+        self.np_dtype = np.float32 if ref.dtype == "f32" else np.float64
+        self.index = {n: i for i, n in enumerate(self.names)}
+        self.grid_cls = type(ref)
+        self.device = default_device() if device is None else device
+        desc = L.DomainDesc()
+        desc.dtype = L.STKB_F32 if ref.dtype == "f32" else L.STKB_F64
+        desc.ndim = nd
+        for d, e in enumerate(self.shape):
+            desc.shape[d] = e
+        desc.order = ref.order
+        desc.n_grids = len(self.names)
+        desc.device = self.device
+        h = ctypes.c_void_p()
+        L.call("stkb_domain_create", ctypes.byref(desc), ctypes.byref(h))
+        self.h = h
+        self._program_key = None
+        self._tags: dict = {}
+        self.plans: list = []  # MapPlan of every compiled map, for inspection
+
+    # -- lifetime --------------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.stkb_domain_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- data ------------------------------------------------------------------
+    def _host(self, arr: np.ndarray) -> np.ndarray:
+        if arr.dtype != self.np_dtype or not arr.flags.c_contiguous:
+            arr = np.ascontiguousarray(arr, dtype=self.np_dtype)
+        return arr
+
+    def upload(self, name: str, data: np.ndarray, sync: bool = True) -> None:
+        arr = self._host(data)
+        fn = "stkb_upload" if sync else "stkb_upload_async"
+        L.call(fn, self.h, self.index[name], arr.ctypes.data_as(ctypes.c_void_p))
+        self._keep = arr
+
+    def download(self, name: str, out: Optional[np.ndarray] = None, sync: bool = True) -> np.ndarray:
+        padded = tuple(e + 2 * self.order for e in self.shape)
+        if out is None:
+            out = np.empty(padded, dtype=self.np_dtype)
+        fn = "stkb_download" if sync else "stkb_download_async"
+        L.call(fn, self.h, self.index[name], out.ctypes.data_as(ctypes.c_void_p))
+        return out
+
+    def layout(self) -> dict:
+        v = [ctypes.c_int64() for _ in range(4)]
+        L.call("stkb_layout", self.h, *[ctypes.byref(x) for x in v])
+        return dict(pitch=v[0].value, plane=v[1].value, lead=v[2].value, elems=v[3].value)
+
+    def device_ptr(self, name: str) -> int:
+        p = ctypes.c_void_p()
+        L.call("stkb_device_ptr", self.h, self.index[name], ctypes.byref(p))
+        return p.value
+
+    def set_stream(self, stream_handle: int) -> None:
+        L.call("stkb_set_stream", self.h, ctypes.c_void_p(stream_handle or None))
+
+    # -- program -----------------------------------------------------------------
+    def compile_map(self, bmap, tag: int, box: Optional[tuple] = None) -> L.MapDesc:
+        try:
+            plan = match_map(bmap, exact=self.precision == "exact")
+        except MatchError as why:
+            raise ExecutionError(f"kernel '{bmap.kernel.name}': {why}") from None
+        self.plans.append(plan)
+        return self.map_desc(plan, tag, box)
+
+    def map_desc(self, plan: MapPlan, tag: int, box: Optional[tuple] = None) -> L.MapDesc:
+        d = L.MapDesc()
+        d.tag = tag
+        d.precision = L.STKB_PREC_FAST
+        d.src = d.dst = d.prev = d.vel = -1
+        bx = box if box is not None else plan.box
+        for i, (lo, hi) in enumerate(bx):
+            d.lo[i], d.hi[i] = lo, hi
+        if plan.kind in ("star", "wave"):
+            d.kind = L.STKB_MAP_STAR if plan.kind == "star" else L.STKB_MAP_WAVE
+            d.radius = plan.radius
+            d.src, d.dst = self.index[plan.src], self.index[plan.dst]
+            if plan.kind == "wave":
+                d.prev, d.vel = self.index[plan.prev], self.index[plan.vel]
+                d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
+            for i, c in enumerate(plan.coef):
+                d.coef[i] = c
+            d.divisor = plan.divisor
+        else:
+            d.kind = L.STKB_MAP_EXPR
+            d.n_args = len(plan.args)
+            for i, g in enumerate(plan.args):
+                d.args[i] = self.index[g]
+            flat = np.ascontiguousarray(np.array(plan.code, dtype=np.int32).reshape(-1))
+            consts = np.ascontiguousarray(np.array(plan.consts if plan.consts else [0.0], dtype=np.float64))
+            d.n_code = len(plan.code)
+            d.code = flat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            d.n_consts = len(plan.consts)
+            d.consts = consts.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            d._keep = (flat, consts)  # alive until stkb_program_add_map copied them
+        return d
+
+    def set_program(self, body: tuple) -> None:
+        """Make ``body`` (maps and swaps) the step program, unless it already is."""
+        key = tuple(id(s) for s in body)  # statements stay alive through self._body
+        if self._program_key == key:
+            return
+        L.call("stkb_program_reset", self.h)
+        self._tags = {}
+        for stmt in body:
+            k = stmt_kind(stmt)
+            if k == "BoundSwap":
+                L.call("stkb_program_add_swap", self.h, self.index[stmt.first], self.index[stmt.second])
+            elif k == "BoundMap":
+                tag = len(self._tags)
+                desc = self.compile_map(stmt, tag)
+                L.call("stkb_program_add_map", self.h, ctypes.byref(desc))
+                self._tags[tag] = stmt.kernel.name
+            else:
+                raise ExecutionError(f"unsupported statement {stmt!r} in a device step program")
+        self._program_key = key
+        self._body = body  # keep the id stable
+
+    def run(self, steps: int) -> None:
+        L.call("stkb_run", self.h, ctypes.c_int64(int(steps)))
+
+    def sync(self) -> None:
+        L.call("stkb_sync", self.h)
+
+    def elapsed_ms(self) -> float:
+        v = ctypes.c_double()
+        L.call("stkb_elapsed_ms", self.h, ctypes.byref(v))
+        return v.value
+
+    def launches(self) -> int:
+        v = ctypes.c_int64()
+        L.call("stkb_launches", self.h, ctypes.byref(v))
+        return v.value
+
+    def check_finite(self) -> None:
+        """Warn per map that produced non-finite values (executor.py:247-253)."""
+        for tag, kname in self._tags.items():
+            f = ctypes.c_int32()
+            L.call("stkb_nonfinite", self.h, tag, ctypes.byref(f))
+            if f.value:
+                warnings.warn(f"kernel '{kname}' produced non-finite values", RuntimeWarning, stacklevel=3)
+
+    # -- statements ----------------------------------------------------------------
+    def execute(self, stmts, bindings: Optional[dict] = None) -> None:
+        bindings = bindings or {}
+        for stmt in stmts:
+            k = stmt_kind(stmt)
+            if k in ("BoundSwap", "BoundMap"):
+                self.set_program((stmt,))
+                self.run(1)
+                self.check_finite()
+            elif k == "BoundFor":
+                count = stmt.count
+                if not isinstance(count, int):
+                    if count not in bindings:
+                        raise ExecutionError(f"runtime loop bound '{count}' is unbound")
+                    count = int(bindings[count])
+                body = tuple(stmt.body)
+                if all(stmt_kind(s) in ("BoundSwap", "BoundMap") for s in body):
+                    if count > 0 and body:
+                        self.set_program(body)
+                        self.run(count)
+                        self.check_finite()
+                else:
+                    for _ in range(count):
+                        self.execute(body, bindings)
+            else:
+                raise ExecutionError(f"unsupported statement {stmt!r}")
+
+
+def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Optional[str] = None,
+            args=None, scheme: Optional[str] = None, *, device: Optional[int] = None,
+            precision: str = "fast") -> dict:
+    """``run_tile_plan`` for GpuPlans, executed on a B200 (executor.py:491-557).
+
+    ``precision="fast"`` runs star/wave maps in the grid dtype on the tuned
+    streaming kernels (fp32 parity tolerance 1e-5 relative);
+    ``precision="exact"`` evaluates every map in float64 in parse order with
+    one rounding per store, bit-identical to ``run_target``.
+    """
+    bound = _prepare(unit, target, args, scheme)
+    check_plan(plan, bound)
+    used = []
+    for bmap in _maps(bound.stmts):
+        for _, g in bmap.grid_args:
+            if g not in used:
+                used.append(g)
+    for g in used:
+        if g not in grids:
+            raise ExecutionError(f"grid '{g}' is not among the supplied grids")
+    out = {n: b.copy() for n, b in grids.items()}
+    if not used:  # only swaps: exchange identities
+        _host_swaps(bound.stmts, out, bindings or {})
+        return out
+    # grids no map touches still take part in swaps: give them device slots too
+    names = used + [n for n in grids if n not in used and _same_layout(grids[n], grids[used[0]])]
+    with DeviceTarget({n: grids[n] for n in names}, names, device=device, precision=precision) as dt:
+        for n in names:
+            dt.upload(n, grids[n].data)
+        dt.execute(bound.stmts, bindings)
+        for n in names:
+            b = out[n]
+            out[n] = type(b)(b.dtype, b.shape, b.order, dt.download(n))
+    return out
+
+
+def _same_layout(a, b) -> bool:
+    return (a.dtype, tuple(a.shape), a.order) == (b.dtype, tuple(b.shape), b.order)
+
+
+def _host_swaps(stmts, state: dict, bindings: dict) -> None:
+    for s in stmts:
+        k = stmt_kind(s)
+        if k == "BoundSwap":
+            state[s.first], state[s.second] = state[s.second], state[s.first]
+        elif k == "BoundFor":
+            count = s.count if isinstance(s.count, int) else int(bindings[s.count])
+            for _ in range(count):
+                _host_swaps(s.body, state, bindings)

@@ -1,0 +1,165 @@
+// Shared device helpers and launch descriptors for the sm_100a stencil kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace stkb {
+
+// ---------------------------------------------------------------------------
+// geometry of a domain's pitched device layout (generalises the reference's
+// IndexScheme, codegen/common.py:14-76: flat(i) = lead_pad + sum (i_d+order)*stride_d
+// with a per-row lead pad and a 128-byte row pitch instead of lead_pad = 0).
+struct Geometry {
+    int64_t n0, n1, n2;   // interior extents
+    int64_t order;        // halo width of d1 and d2
+    int64_t order0;       // halo width of d0 (== order for 3-D grids; 0 for 2-D grids lifted to 3-D)
+    int64_t pitch;        // elements per padded row (multiple of 128 B)
+    int64_t plane;        // elements per padded plane = pitch * (n1 + 2*order)
+    int64_t lead;         // column of interior x = 0 within a row (128 B)
+    // flat element index of interior coordinate (z, y, x)
+    __host__ __device__ __forceinline__ int64_t at(int64_t z, int64_t y, int64_t x) const {
+        return (z + order0) * plane + (y + order) * pitch + lead + x;
+    }
+};
+
+struct Box {
+    int32_t lo0, hi0, lo1, hi1, lo2, hi2;
+};
+
+// Arguments of the 2.5D streaming star kernel (STAR and WAVE forms).
+template <typename T>
+struct StarArgs {
+    Geometry g;
+    Box box;
+    int32_t x0base;            // lo2 rounded down to the vector width
+    int32_t n_tx, n_ty, n_tz;  // work-item grid: x tiles, y tiles, z chunks
+    int32_t lz;                // z-chunk length
+    int32_t n_items;
+    T* dst;
+    const T* src;              // centre re-read (WAVE)
+    const T* prev;             // WAVE
+    const T* vel;              // WAVE
+    int32_t* nonfinite;        // sticky flag
+    T c0;                      // centre
+    T cm[3][4];                // [axis][m-1] coefficient of offset -m
+    T cp[3][4];                // [axis][m-1] coefficient of offset +m
+    T divisor;
+    T wave_a, wave_b;
+};
+
+// ---------------------------------------------------------------------------
+// mbarrier / TMA PTX wrappers (sm_90+ ISA, used here for sm_100a)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// 3-D tiled TMA load global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+          "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// vector types: 16 bytes per access
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ void load16(const T* p, T (&v)[16 / sizeof(T)]) {
+    using V = typename Vec16<T>::type;
+    V t = *reinterpret_cast<const V*>(p);
+    if constexpr (sizeof(T) == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
+    else { v[0] = t.x; v[1] = t.y; }
+}
+
+// streaming global loads of read-once centre values (WAVE: prev, vel)
+template <typename T>
+__device__ __forceinline__ void ldg_stream16(const T* p, T (&v)[16 / sizeof(T)]) {
+    if constexpr (sizeof(T) == 4) {
+        float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+        double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void ldg16(const T* p, T (&v)[16 / sizeof(T)]) {
+    if constexpr (sizeof(T) == 4) {
+        float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+        double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void stg16(T* p, const T (&v)[16 / sizeof(T)]) {
+    if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    }
+}
+
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+}  // namespace stkb
+
+// host-side launchers implemented per dtype (star_f32.cu / star_f64.cu)
+namespace stkb {
+struct StarLaunch {
+    int kind;          // 1 = STAR, 2 = WAVE
+    int radius;
+    bool has_divisor;
+    const CUtensorMap* maps;  // [4]: src halo box, src centre box, prev centre box, vel centre box
+    int num_sms;
+    int max_ctas;      // 0 = auto (one per SM)
+    int lz;            // 0 = auto
+};
+int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
+cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
+cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
+}  // namespace stkb

@@ -1,0 +1,698 @@
+// libstkb200: the C-ABI (include/stkb200.h) over the sm_100a kernels.
+//
+// A domain owns the pitched device copies of one target's grids, a stream, the
+// TMA tensor maps of every buffer, and a step program (maps + swaps) that it
+// replays through a CUDA graph.  The name -> buffer binding follows the
+// reference's swap semantics (executor.py:229-230): a swap is free, it only
+// exchanges which device buffer a grid name denotes.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/stkb200.h"
+#include "common.cuh"
+
+namespace stkb {
+cudaError_t launch_expr(int dtype, const Geometry& g, const Box& box, const int32_t* code,
+                        const double* consts, int n_code, int n_args, const void* const* rd,
+                        void* const* wr, int32_t* flag, int num_sms, cudaStream_t s);
+cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const void* got, void* partials,
+                           int blocks, cudaStream_t s);
+size_t compare_partial_bytes();
+}  // namespace stkb
+
+using namespace stkb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(STKB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int kMaxTags = 64;
+
+struct MapOp {
+    stkb_map_desc d;
+    std::vector<int32_t> code;
+    std::vector<double> consts;
+    int32_t* d_code = nullptr;
+    double* d_consts = nullptr;
+    bool snapshot[STKB_EXPR_MAX_ARGS] = {};  // EXPR: arg written and read -> read a copy
+};
+
+struct ProgOp {
+    int kind;  // 0 = map, 1 = swap
+    int map;
+    int a, b;
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encoder() {
+    if (g_encode) return STKB_OK;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+        return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return STKB_OK;
+}
+
+}  // namespace
+
+struct stkb_domain {
+    stkb_domain_desc desc{};
+    Geometry g{};
+    size_t elem = 4;
+    int num_sms = 148;
+    std::vector<void*> bufs;
+    std::vector<void*> snap;  // snapshot buffers for EXPR maps (lazily)
+    std::vector<int32_t> binding;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::vector<MapOp> maps;
+    std::vector<ProgOp> prog;
+    std::map<std::tuple<int, int, int>, CUtensorMap> tmaps;  // (buffer, box w, box h)
+    // graph cache: start binding -> (exec of `period` steps, kernels per replay)
+    std::map<std::vector<int32_t>, std::pair<cudaGraphExec_t, int64_t>> graphs;
+    int gperiod = 0;
+    bool warmed = false;  // one direct step ran since the program changed
+    // timing
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;
+    int64_t last_launches = 0;
+    int32_t* d_flags = nullptr;
+    void* d_partials = nullptr;
+    int lz_override = 0;
+    int ctas_override = 0;
+};
+
+namespace {
+
+int encode_map(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap** out) {
+    auto key = std::make_tuple(buffer, bw, bh);
+    auto it = dom->tmaps.find(key);
+    if (it != dom->tmaps.end()) {
+        *out = &it->second;
+        return STKB_OK;
+    }
+    int rc = get_encoder();
+    if (rc) return rc;
+    CUtensorMap m;
+    const Geometry& g = dom->g;
+    cuuint64_t dims[3] = {cuuint64_t(g.pitch), cuuint64_t(g.n1 + 2 * g.order), cuuint64_t(g.n0 + 2 * g.order0)};
+    cuuint64_t strides[2] = {cuuint64_t(g.pitch * dom->elem), cuuint64_t(g.plane * dom->elem)};
+    cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(bh), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(&m, dom->elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                          3, dom->bufs[buffer], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    auto res = dom->tmaps.emplace(key, m);
+    *out = &res.first->second;
+    return STKB_OK;
+}
+
+Box box_of(const stkb_map_desc& d) {
+    Box b;
+    b.lo0 = int32_t(d.lo[0]); b.hi0 = int32_t(d.hi[0]);
+    b.lo1 = int32_t(d.lo[1]); b.hi1 = int32_t(d.hi[1]);
+    b.lo2 = int32_t(d.lo[2]); b.hi2 = int32_t(d.hi[2]);
+    return b;
+}
+
+template <typename T>
+int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind) {
+    const stkb_map_desc& d = op.d;
+    StarArgs<T> a{};
+    a.g = dom->g;
+    a.box = box_of(d);
+    constexpr int VEC = 16 / sizeof(T);
+    a.x0base = a.box.lo2 - (a.box.lo2 % VEC);
+    const int sb = bind[d.src];
+    a.dst = static_cast<T*>(dom->bufs[bind[d.dst]]);
+    a.src = static_cast<const T*>(dom->bufs[sb]);
+    a.prev = d.prev >= 0 ? static_cast<const T*>(dom->bufs[bind[d.prev]]) : nullptr;
+    a.vel = d.vel >= 0 ? static_cast<const T*>(dom->bufs[bind[d.vel]]) : nullptr;
+    a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
+    const int R = d.radius;
+    a.c0 = T(d.coef[0]);
+    for (int ax = 0; ax < 3; ++ax)
+        for (int m = 1; m <= 4; ++m) {
+            a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)]) : T(0);
+            a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1]) : T(0);
+        }
+    a.divisor = T(d.divisor);
+    a.wave_a = T(d.wave_a);
+    a.wave_b = T(d.wave_b);
+
+    int bx, by, hx;
+    star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
+    const CUtensorMap* m_halo = nullptr;
+    int rc = encode_map(dom, sb, bx + 2 * hx, by + 2 * R, &m_halo);
+    if (rc) return rc;
+    CUtensorMap maps[4];
+    maps[0] = *m_halo;
+    maps[1] = maps[2] = maps[3] = *m_halo;
+    if (d.kind == STKB_MAP_WAVE) {
+        const CUtensorMap *mc, *mp, *mv;
+        if ((rc = encode_map(dom, sb, bx, by, &mc))) return rc;
+        if ((rc = encode_map(dom, bind[d.prev], bx, by, &mp))) return rc;
+        if ((rc = encode_map(dom, bind[d.vel], bx, by, &mv))) return rc;
+        maps[1] = *mc;
+        maps[2] = *mp;
+        maps[3] = *mv;
+    }
+    StarLaunch L{};
+    L.kind = d.kind;
+    L.radius = R;
+    L.has_divisor = d.divisor != 0.0;
+    L.maps = maps;
+    L.num_sms = dom->num_sms;
+    L.max_ctas = dom->ctas_override;
+    L.lz = dom->lz_override;
+    cudaError_t e;
+    if constexpr (sizeof(T) == 4) e = launch_star_f32(L, a, dom->stream);
+    else e = launch_star_f64(L, a, dom->stream);
+    if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("star kernel launch: ") + cudaGetErrorString(e));
+    return STKB_OK;
+}
+
+int launch_expr_map(stkb_domain* dom, MapOp& op, const std::vector<int32_t>& bind) {
+    const stkb_map_desc& d = op.d;
+    const void* rd[STKB_EXPR_MAX_ARGS];
+    void* wr[STKB_EXPR_MAX_ARGS];
+    const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
+    for (int i = 0; i < d.n_args; ++i) {
+        void* b = dom->bufs[bind[d.args[i]]];
+        wr[i] = b;
+        rd[i] = b;
+        if (op.snapshot[i]) {
+            // the oracle snapshots every grid before a map (executor.py:66-69)
+            CUDA_TRY(cudaMemcpyAsync(dom->snap[i], b, bytes, cudaMemcpyDeviceToDevice, dom->stream));
+            rd[i] = dom->snap[i];
+        }
+    }
+    cudaError_t e = launch_expr(dom->desc.dtype, dom->g, box_of(d), op.d_code, op.d_consts, int(op.code.size() / 5),
+                                d.n_args, rd, wr, dom->d_flags + (d.tag & (kMaxTags - 1)), dom->num_sms,
+                                dom->stream);
+    if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("expr kernel launch: ") + cudaGetErrorString(e));
+    return STKB_OK;
+}
+
+// enqueue one step of the program starting from `bind`; updates `bind`
+int enqueue_step(stkb_domain* dom, std::vector<int32_t>& bind, int64_t* launches) {
+    for (const ProgOp& p : dom->prog) {
+        if (p.kind == 1) {
+            std::swap(bind[p.a], bind[p.b]);
+            continue;
+        }
+        MapOp& op = dom->maps[p.map];
+        int rc;
+        if (op.d.kind == STKB_MAP_EXPR) rc = launch_expr_map(dom, op, bind);
+        else if (dom->desc.dtype == STKB_F32) rc = launch_star_map<float>(dom, op, bind);
+        else rc = launch_star_map<double>(dom, op, bind);
+        if (rc) return rc;
+        ++*launches;
+    }
+    return STKB_OK;
+}
+
+void invalidate_graph(stkb_domain* dom) {
+    for (auto& kv : dom->graphs) cudaGraphExecDestroy(kv.second.first);
+    dom->graphs.clear();
+    dom->gperiod = 0;
+    dom->warmed = false;
+}
+
+// period of the binding permutation induced by one step
+int binding_period(const stkb_domain* dom) {
+    std::vector<int32_t> b(dom->binding.size());
+    for (size_t i = 0; i < b.size(); ++i) b[i] = int32_t(i);
+    std::vector<int32_t> cur = b;
+    for (int k = 1; k <= 16; ++k) {
+        for (const ProgOp& p : dom->prog)
+            if (p.kind == 1) std::swap(cur[p.a], cur[p.b]);
+        if (cur == b) return k;
+    }
+    return 0;
+}
+
+int check_name(const stkb_domain* dom, int32_t n, const char* what) {
+    if (n < 0 || n >= dom->desc.n_grids) return fail(STKB_ERR_ARG, std::string(what) + ": grid name index out of range");
+    return STKB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stkb_abi_version(void) { return STKB_ABI_VERSION; }
+
+const char* stkb_last_error(void) { return g_err.c_str(); }
+
+int stkb_device_count(int32_t* count) {
+    int n = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n));
+    *count = n;
+    return STKB_OK;
+}
+
+int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
+    if (!desc || !out) return fail(STKB_ERR_ARG, "null argument");
+    if (desc->dtype != STKB_F32 && desc->dtype != STKB_F64) return fail(STKB_ERR_ARG, "dtype must be STKB_F32 or STKB_F64");
+    if (desc->ndim != 2 && desc->ndim != 3) return fail(STKB_ERR_UNSUPPORTED, "only 2-D and 3-D grids are supported");
+    if (desc->n_grids < 1 || desc->n_grids > 32) return fail(STKB_ERR_ARG, "n_grids must be in 1..32");
+    if (desc->order < 0 || desc->order > 16) return fail(STKB_ERR_ARG, "order must be in 0..16");
+    for (int d = 0; d < desc->ndim; ++d)
+        if (desc->shape[d] < 1 || desc->shape[d] > (1 << 24)) return fail(STKB_ERR_ARG, "extent out of range");
+    CUDA_TRY(cudaSetDevice(desc->device));
+    auto* dom = new stkb_domain();
+    dom->desc = *desc;
+    dom->elem = desc->dtype == STKB_F32 ? 4 : 8;
+    const int64_t per128 = 128 / int64_t(dom->elem);
+    Geometry& g = dom->g;
+    if (desc->ndim == 3) {
+        g.n0 = desc->shape[0]; g.n1 = desc->shape[1]; g.n2 = desc->shape[2];
+        g.order0 = desc->order;
+    } else {  // 2-D grids are lifted to a single d0 plane without d0 halo
+        g.n0 = 1; g.n1 = desc->shape[0]; g.n2 = desc->shape[1];
+        g.order0 = 0;
+    }
+    g.order = desc->order;
+    g.lead = std::max<int64_t>(per128, ((desc->order + per128 - 1) / per128) * per128);
+    g.pitch = ((g.lead + g.n2 + g.order + per128 - 1) / per128) * per128;
+    g.plane = g.pitch * (g.n1 + 2 * g.order);
+    const size_t bytes = size_t(g.plane) * size_t(g.n0 + 2 * g.order0) * dom->elem;
+    int dev = desc->device;
+    cudaDeviceGetAttribute(&dom->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    dom->bufs.assign(desc->n_grids, nullptr);
+    dom->snap.assign(STKB_EXPR_MAX_ARGS, nullptr);
+    dom->binding.resize(desc->n_grids);
+    for (int i = 0; i < desc->n_grids; ++i) dom->binding[i] = i;
+    auto cleanup = [&](const std::string& msg) {
+        stkb_domain_destroy(dom);
+        return fail(STKB_ERR_CUDA, msg);
+    };
+    for (int i = 0; i < desc->n_grids; ++i) {
+        cudaError_t e = cudaMalloc(&dom->bufs[i], bytes);
+        if (e != cudaSuccess) return cleanup(std::string("cudaMalloc grid buffer: ") + cudaGetErrorString(e));
+        e = cudaMemset(dom->bufs[i], 0, bytes);
+        if (e != cudaSuccess) return cleanup(std::string("cudaMemset: ") + cudaGetErrorString(e));
+    }
+    if (cudaStreamCreateWithFlags(&dom->own_stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup("stream");
+    dom->stream = dom->own_stream;
+    if (cudaEventCreate(&dom->ev0) != cudaSuccess || cudaEventCreate(&dom->ev1) != cudaSuccess) return cleanup("event");
+    if (cudaMalloc(&dom->d_flags, kMaxTags * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
+    cudaMemset(dom->d_flags, 0, kMaxTags * sizeof(int32_t));
+    if (const char* s = getenv("STKB_LZ")) dom->lz_override = atoi(s);
+    if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
+    *out = dom;
+    return STKB_OK;
+}
+
+int stkb_domain_destroy(stkb_domain* dom) {
+    if (!dom) return STKB_OK;
+    cudaSetDevice(dom->desc.device);
+    if (dom->stream) cudaStreamSynchronize(dom->stream);
+    invalidate_graph(dom);
+    for (auto& m : dom->maps) {
+        if (m.d_code) cudaFree(m.d_code);
+        if (m.d_consts) cudaFree(m.d_consts);
+    }
+    for (void* b : dom->bufs) if (b) cudaFree(b);
+    for (void* b : dom->snap) if (b) cudaFree(b);
+    if (dom->d_flags) cudaFree(dom->d_flags);
+    if (dom->d_partials) cudaFree(dom->d_partials);
+    if (dom->ev0) cudaEventDestroy(dom->ev0);
+    if (dom->ev1) cudaEventDestroy(dom->ev1);
+    if (dom->own_stream) cudaStreamDestroy(dom->own_stream);
+    delete dom;
+    return STKB_OK;
+}
+
+int stkb_layout(const stkb_domain* dom, int64_t* pitch, int64_t* plane, int64_t* lead, int64_t* elems) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (pitch) *pitch = dom->g.pitch;
+    if (plane) *plane = dom->g.plane;
+    if (lead) *lead = dom->g.lead;
+    if (elems) *elems = dom->g.plane * (dom->g.n0 + 2 * dom->g.order0);
+    return STKB_OK;
+}
+
+int stkb_device_ptr(stkb_domain* dom, int32_t name, void** dptr) {
+    if (!dom || !dptr) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_device_ptr")) return rc;
+    *dptr = dom->bufs[dom->binding[name]];
+    return STKB_OK;
+}
+
+int stkb_set_stream(stkb_domain* dom, void* stream) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->stream = stream ? static_cast<cudaStream_t>(stream) : dom->own_stream;
+    return STKB_OK;
+}
+
+static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
+    if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_upload")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    const Geometry& g = dom->g;
+    const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
+    char* dst = static_cast<char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
+    CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(g.pitch) * dom->elem, host, row, row,
+                               size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order), cudaMemcpyHostToDevice,
+                               dom->stream));
+    return STKB_OK;
+}
+
+static int copy_d2h(stkb_domain* dom, int32_t name, void* host) {
+    if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_download")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    const Geometry& g = dom->g;
+    const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
+    const char* src = static_cast<const char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
+    CUDA_TRY(cudaMemcpy2DAsync(host, row, src, size_t(g.pitch) * dom->elem, row,
+                               size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order), cudaMemcpyDeviceToHost,
+                               dom->stream));
+    return STKB_OK;
+}
+
+int stkb_upload_async(stkb_domain* dom, int32_t name, const void* host) { return copy_h2d(dom, name, host); }
+int stkb_download_async(stkb_domain* dom, int32_t name, void* host) { return copy_d2h(dom, name, host); }
+
+int stkb_upload(stkb_domain* dom, int32_t name, const void* host) {
+    if (int rc = copy_h2d(dom, name, host)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_download(stkb_domain* dom, int32_t name, void* host) {
+    if (int rc = copy_d2h(dom, name, host)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_program_reset(stkb_domain* dom) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    cudaSetDevice(dom->desc.device);
+    cudaStreamSynchronize(dom->stream);
+    invalidate_graph(dom);
+    for (auto& m : dom->maps) {
+        if (m.d_code) cudaFree(m.d_code);
+        if (m.d_consts) cudaFree(m.d_consts);
+    }
+    dom->maps.clear();
+    dom->prog.clear();
+    return STKB_OK;
+}
+
+int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
+    if (!dom || !md) return fail(STKB_ERR_ARG, "null argument");
+    const stkb_map_desc& d = *md;
+    const Geometry& g = dom->g;
+    const int nd = dom->desc.ndim;
+    // region box in lifted 3-D interior coordinates
+    int64_t lo[3], hi[3];
+    if (nd == 3) {
+        for (int i = 0; i < 3; ++i) { lo[i] = d.lo[i]; hi[i] = d.hi[i]; }
+    } else {
+        lo[0] = 0; hi[0] = 1;
+        lo[1] = d.lo[0]; hi[1] = d.hi[0];
+        lo[2] = d.lo[1]; hi[2] = d.hi[1];
+    }
+    const int64_t ext[3] = {g.n0, g.n1, g.n2};
+    for (int i = 0; i < 3; ++i)
+        if (lo[i] < 0 || hi[i] > ext[i] || lo[i] > hi[i])
+            return fail(STKB_ERR_ARG, "map region outside the interior");
+    MapOp op;
+    op.d = d;
+    for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
+    if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE) {
+        if (nd != 3) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels need a 3-D grid");
+        if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
+        if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");
+        if (int rc = check_name(dom, d.src, "src")) return rc;
+        if (int rc = check_name(dom, d.dst, "dst")) return rc;
+        if (d.src == d.dst) return fail(STKB_ERR_ARG, "star map reads and writes the same grid (needs a snapshot: use EXPR)");
+        if (d.kind == STKB_MAP_WAVE) {
+            if (int rc = check_name(dom, d.prev, "prev")) return rc;
+            if (int rc = check_name(dom, d.vel, "vel")) return rc;
+            if (d.vel == d.dst) return fail(STKB_ERR_ARG, "wave map writes its velocity grid");
+        }
+        if (d.precision != STKB_PREC_FAST) return fail(STKB_ERR_UNSUPPORTED, "unknown precision");
+    } else if (d.kind == STKB_MAP_EXPR) {
+        if (d.n_args < 1 || d.n_args > STKB_EXPR_MAX_ARGS) return fail(STKB_ERR_ARG, "EXPR map: n_args out of range");
+        if (d.n_code < 1 || !d.code) return fail(STKB_ERR_ARG, "EXPR map: empty code");
+        for (int i = 0; i < d.n_args; ++i)
+            if (int rc = check_name(dom, d.args[i], "EXPR arg")) return rc;
+        op.code.assign(d.code, d.code + 5 * size_t(d.n_code));
+        op.consts.assign(d.consts, d.consts + std::max(0, d.n_consts));
+        // static checks: stack discipline, argument indices, halo-safe offsets
+        bool written[STKB_EXPR_MAX_ARGS] = {}, read[STKB_EXPR_MAX_ARGS] = {};
+        int sp = 0, maxsp = 0;
+        const int64_t o0 = g.order0, o = g.order;
+        for (int pc = 0; pc < d.n_code; ++pc) {
+            const int32_t* ins = &op.code[5 * pc];
+            int32_t oz = ins[2], oy = ins[3], ox = ins[4];
+            if (nd == 2 && (ins[0] == STKB_OP_READ || ins[0] == STKB_OP_STORE)) { ox = ins[3]; oy = ins[2]; oz = 0; }
+            switch (ins[0]) {
+                case STKB_OP_CONST:
+                    if (ins[1] < 0 || ins[1] >= d.n_consts) return fail(STKB_ERR_ARG, "EXPR: const index");
+                    ++sp; break;
+                case STKB_OP_READ:
+                case STKB_OP_STORE:
+                    if (ins[1] < 0 || ins[1] >= d.n_args) return fail(STKB_ERR_ARG, "EXPR: arg index");
+                    if (lo[0] + oz < -o0 || hi[0] - 1 + oz >= g.n0 + o0 || lo[1] + oy < -o ||
+                        hi[1] - 1 + oy >= g.n1 + o || lo[2] + ox < -o || hi[2] - 1 + ox >= g.n2 + o)
+                        return fail(STKB_ERR_ARG, "EXPR: offset reaches beyond the halo");
+                    if (ins[0] == STKB_OP_READ) { read[ins[1]] = true; ++sp; }
+                    else {
+                        if (lo[0] + oz < 0 || hi[0] - 1 + oz >= g.n0 || lo[1] + oy < 0 || hi[1] - 1 + oy >= g.n1 ||
+                            lo[2] + ox < 0 || hi[2] - 1 + ox >= g.n2)
+                            return fail(STKB_ERR_ARG, "update destination offset writes outside the interior");
+                        written[ins[1]] = true; --sp;
+                    }
+                    // lift 2-D offsets into the 3-D lane layout the kernel reads
+                    op.code[5 * pc + 2] = oz; op.code[5 * pc + 3] = oy; op.code[5 * pc + 4] = ox;
+                    break;
+                case STKB_OP_LOCAL:
+                    if (ins[1] < 0 || ins[1] >= STKB_EXPR_MAX_LOCALS) return fail(STKB_ERR_ARG, "EXPR: local index");
+                    ++sp; break;
+                case STKB_OP_SETLOCAL:
+                    if (ins[1] < 0 || ins[1] >= STKB_EXPR_MAX_LOCALS) return fail(STKB_ERR_ARG, "EXPR: local index");
+                    --sp; break;
+                case STKB_OP_ADD: case STKB_OP_SUB: case STKB_OP_MUL: case STKB_OP_DIV: --sp; break;
+                case STKB_OP_NEG: break;
+                default: return fail(STKB_ERR_ARG, "EXPR: unknown opcode");
+            }
+            if (sp < 0) return fail(STKB_ERR_ARG, "EXPR: stack underflow");
+            maxsp = std::max(maxsp, sp);
+        }
+        if (sp != 0) return fail(STKB_ERR_ARG, "EXPR: unbalanced stack");
+        if (maxsp > STKB_EXPR_MAX_STACK) return fail(STKB_ERR_UNSUPPORTED, "EXPR: expression too deep");
+        // a grid that is both read and written is read from a pre-map copy,
+        // and aliases (the same name bound to several params) share one
+        for (int i = 0; i < d.n_args; ++i) {
+            bool w = false, r = false;
+            for (int j = 0; j < d.n_args; ++j)
+                if (d.args[j] == d.args[i]) { w |= written[j]; r |= read[j]; }
+            op.snapshot[i] = w && r;
+        }
+        CUDA_TRY(cudaSetDevice(dom->desc.device));
+        const size_t gbytes = size_t(g.plane) * size_t(g.n0 + 2 * g.order0) * dom->elem;
+        for (int i = 0; i < d.n_args; ++i)
+            if (op.snapshot[i] && !dom->snap[i]) CUDA_TRY(cudaMalloc(&dom->snap[i], gbytes));
+        CUDA_TRY(cudaMalloc(&op.d_code, op.code.size() * sizeof(int32_t)));
+        CUDA_TRY(cudaMemcpy(op.d_code, op.code.data(), op.code.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        const size_t nc = std::max<size_t>(1, op.consts.size());
+        CUDA_TRY(cudaMalloc(&op.d_consts, nc * sizeof(double)));
+        if (!op.consts.empty())
+            CUDA_TRY(cudaMemcpy(op.d_consts, op.consts.data(), op.consts.size() * sizeof(double), cudaMemcpyHostToDevice));
+        op.d.code = nullptr;
+        op.d.consts = nullptr;
+    } else {
+        return fail(STKB_ERR_ARG, "unknown map kind");
+    }
+    invalidate_graph(dom);
+    dom->maps.push_back(std::move(op));
+    dom->prog.push_back(ProgOp{0, int(dom->maps.size()) - 1, 0, 0});
+    return STKB_OK;
+}
+
+int stkb_program_add_swap(stkb_domain* dom, int32_t a, int32_t b) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (int rc = check_name(dom, a, "swap")) return rc;
+    if (int rc = check_name(dom, b, "swap")) return rc;
+    invalidate_graph(dom);
+    dom->prog.push_back(ProgOp{1, -1, a, b});
+    return STKB_OK;
+}
+
+int stkb_run(stkb_domain* dom, int64_t steps) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (steps < 0) return fail(STKB_ERR_ARG, "negative step count");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
+    int64_t launches = 0;
+    int64_t done = 0;
+    const int period = binding_period(dom);
+    const bool graphs_ok = period > 0 && getenv("STKB_NO_GRAPH") == nullptr;
+    // the first step after a program change runs uncaptured: it sets kernel
+    // attributes and encodes tensor maps outside any capture
+    if (graphs_ok && !dom->warmed && steps > 0) {
+        if (int rc = enqueue_step(dom, dom->binding, &launches)) return rc;
+        dom->warmed = true;
+        done = 1;
+    }
+    if (graphs_ok && steps - done >= period) {
+        auto it = dom->graphs.find(dom->binding);
+        if (it == dom->graphs.end()) {
+            cudaStream_t cap = dom->stream;
+            CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            std::vector<int32_t> b = dom->binding;
+            int64_t n = 0;
+            int rc = STKB_OK;
+            for (int k = 0; k < period && rc == STKB_OK; ++k) rc = enqueue_step(dom, b, &n);
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamEndCapture(cap, &graph);
+            if (rc) {
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+            cudaGraphExec_t ex = nullptr;
+            e = cudaGraphInstantiate(&ex, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+            it = dom->graphs.emplace(dom->binding, std::make_pair(ex, n)).first;
+            dom->gperiod = period;
+        }
+        const int64_t reps = (steps - done) / period;
+        for (int64_t r = 0; r < reps; ++r) CUDA_TRY(cudaGraphLaunch(it->second.first, dom->stream));
+        launches += reps * it->second.second;
+        done += reps * period;  // the binding is back where it started
+    }
+    for (; done < steps; ++done)
+        if (int rc = enqueue_step(dom, dom->binding, &launches)) return rc;
+    CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
+    dom->timed = true;
+    dom->last_launches = launches;
+    return STKB_OK;
+}
+
+int stkb_run_once(stkb_domain* dom) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    int64_t launches = 0;
+    CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
+    if (int rc = enqueue_step(dom, dom->binding, &launches)) return rc;
+    CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
+    dom->timed = true;
+    dom->last_launches = launches;
+    return STKB_OK;
+}
+
+int stkb_sync(stkb_domain* dom) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_elapsed_ms(stkb_domain* dom, double* ms) {
+    if (!dom || !ms) return fail(STKB_ERR_ARG, "null argument");
+    if (!dom->timed) return fail(STKB_ERR_STATE, "no run recorded");
+    CUDA_TRY(cudaEventSynchronize(dom->ev1));
+    float f = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&f, dom->ev0, dom->ev1));
+    *ms = f;
+    return STKB_OK;
+}
+
+int stkb_launches(stkb_domain* dom, int64_t* count) {
+    if (!dom || !count) return fail(STKB_ERR_ARG, "null argument");
+    *count = dom->last_launches;
+    return STKB_OK;
+}
+
+int stkb_binding(const stkb_domain* dom, int32_t name, int32_t* buffer) {
+    if (!dom || !buffer) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_binding")) return rc;
+    *buffer = dom->binding[name];
+    return STKB_OK;
+}
+
+int stkb_nonfinite(stkb_domain* dom, int32_t tag, int32_t* flag) {
+    if (!dom || !flag) return fail(STKB_ERR_ARG, "null argument");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    int32_t* p = dom->d_flags + (tag & (kMaxTags - 1));
+    CUDA_TRY(cudaMemcpyAsync(flag, p, sizeof(int32_t), cudaMemcpyDeviceToHost, dom->stream));
+    CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(int32_t), dom->stream));
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_run_target(stkb_domain* dom, void* const* host, int64_t iters) {
+    if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
+    for (int i = 0; i < dom->desc.n_grids; ++i)
+        if (int rc = copy_h2d(dom, i, host[i])) return rc;
+    if (int rc = stkb_run(dom, iters)) return rc;
+    for (int i = 0; i < dom->desc.n_grids; ++i)
+        if (int rc = copy_d2h(dom, i, host[i])) return rc;
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_compare(stkb_domain* dom, int32_t a, int32_t b, double* max_err, double* sum_sq, int64_t* worst,
+                 double* scale) {
+    if (!dom || !max_err || !sum_sq || !worst || !scale) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, a, "compare")) return rc;
+    if (int rc = check_name(dom, b, "compare")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    const int blocks = dom->num_sms * 4;
+    const size_t pb = compare_partial_bytes();
+    if (!dom->d_partials) CUDA_TRY(cudaMalloc(&dom->d_partials, blocks * pb));
+    CUDA_TRY(launch_compare(dom->desc.dtype, dom->g, dom->bufs[dom->binding[a]], dom->bufs[dom->binding[b]],
+                            dom->d_partials, blocks, dom->stream));
+    std::vector<unsigned char> host(blocks * pb);
+    CUDA_TRY(cudaMemcpyAsync(host.data(), dom->d_partials, blocks * pb, cudaMemcpyDeviceToHost, dom->stream));
+    CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    struct P { double max_err, sum_sq, scale; long long worst; };
+    double me = 0, ss = 0, sc = 0;
+    long long w = -1;
+    for (int i = 0; i < blocks; ++i) {
+        P p;
+        memcpy(&p, host.data() + i * pb, sizeof(P));
+        if (p.worst >= 0 && (w < 0 || p.max_err > me || (p.max_err == me && p.worst < w))) { me = p.max_err; w = p.worst; }
+        ss += p.sum_sq;
+        sc = std::max(sc, p.scale);
+    }
+    *max_err = me;
+    *sum_sq = ss;
+    *worst = w;
+    *scale = sc;
+    return STKB_OK;
+}
+
+}  // extern "C"

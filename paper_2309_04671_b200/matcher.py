@@ -1,0 +1,341 @@
+"""Kernel matcher: BoundMap -> one C-ABI map descriptor.
+
+Decides which device kernel evaluates a bound map and extracts its
+parameters.  The reference's own term collection for additive kernels is the
+pattern (``split_semi_terms`` / ``peel_constant_divisor``, executor.py:149-188):
+here the update expression is expanded into a polynomial over grid reads
+(constants folded in float64) and matched against
+
+  STAR  v[0] = (sum_k c_k * u[o_k]) [/ d]      star offsets, radius 1..4, 3-D
+  WAVE  w[0] = a*u[0] + b*p[0] + k[0] * (sum_k c_k * u[o_k])
+
+Everything else — box/"other" shapes, locals, several updates, 2-D maps,
+in-place Jacobi updates, offset destinations, or ``precision="exact"`` —
+compiles to EXPR bytecode, which the device evaluates in float64 in parse
+order with one rounding per store (bit-identical to run_target).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+from .program import node_kind
+
+MAX_FAST_RADIUS = 4
+
+
+class MatchError(ValueError):
+    pass
+
+
+@dataclass
+class MapPlan:
+    kind: str  # "star" | "wave" | "expr"
+    radius: int = 0
+    src: Optional[str] = None  # module grid names
+    dst: Optional[str] = None
+    prev: Optional[str] = None
+    vel: Optional[str] = None
+    coef: list = field(default_factory=list)  # 6R+1, C-ABI layout
+    divisor: float = 0.0
+    wave_a: float = 0.0
+    wave_b: float = 0.0
+    box: tuple = ()  # ((lo, hi), ...) interior coordinates
+    # EXPR
+    args: list = field(default_factory=list)  # module grid name per kernel grid param
+    code: list = field(default_factory=list)  # [op, a, b, c, d] * n
+    consts: list = field(default_factory=list)
+    reason: str = ""  # why the fast path was not taken
+
+
+def coef_index(offset: tuple, radius: int) -> int:
+    """Slot of a star offset in the C-ABI coefficient table."""
+    nz = [(a, c) for a, c in enumerate(offset) if c]
+    if not nz:
+        return 0
+    (axis, c), = nz
+    return 1 + axis * 2 * radius + 2 * (abs(c) - 1) + (1 if c > 0 else 0)
+
+
+# ---------------------------------------------------------------------------
+# polynomial expansion (fast-path matching only; evaluation order is not kept)
+
+
+def _mul(p: dict, q: dict) -> dict:
+    out: dict = {}
+    for ka, va in p.items():
+        for kb, vb in q.items():
+            key = tuple(sorted(ka + kb))
+            if len(key) > 2:
+                raise MatchError("expression is not of degree <= 2 in grid reads")
+            out[key] = out.get(key, 0.0) + va * vb
+    return out
+
+
+def _add(p: dict, q: dict, sign: float = 1.0) -> dict:
+    out = dict(p)
+    for k, v in q.items():
+        out[k] = out.get(k, 0.0) + sign * v
+    return out
+
+
+def expand(expr, locals_: dict, scalars: dict) -> dict:
+    """Polynomial {(read, ...): coefficient}; a read is (grid param, offset)."""
+    k = node_kind(expr)
+    if k == "Const":
+        return {(): float(expr.value)}
+    if k == "Read":
+        return {((expr.grid, tuple(expr.offset)),): 1.0}
+    if k == "Var":
+        if expr.name in locals_:
+            return locals_[expr.name]
+        if expr.name in scalars:
+            return {(): float(scalars[expr.name])}
+        raise MatchError(f"unbound name '{expr.name}' in kernel expression")
+    if k == "Unary":
+        return {kk: -v for kk, v in expand(expr.operand, locals_, scalars).items()}
+    if k == "Binary":
+        a = expand(expr.left, locals_, scalars)
+        b = expand(expr.right, locals_, scalars)
+        if expr.op == "+":
+            return _add(a, b)
+        if expr.op == "-":
+            return _add(a, b, -1.0)
+        if expr.op == "*":
+            return _mul(a, b)
+        if set(b) == {()}:
+            return {kk: v / b[()] for kk, v in a.items()}
+        raise MatchError("division by a grid-dependent expression")
+    raise MatchError(f"unsupported expression node {k}")
+
+
+def _drop_zeros(p: dict) -> dict:
+    return {k: v for k, v in p.items() if v != 0.0}
+
+
+def _is_star(offsets, dims: int) -> bool:
+    return all(len(o) == dims and sum(1 for c in o if c) <= 1 for o in offsets)
+
+
+# ---------------------------------------------------------------------------
+
+
+def map_box(bmap) -> tuple:
+    """Union box of a map's regions; they are an exact cover of it
+    (analysis.py:322-376), and every region evaluates the same expression
+    against the same pre-map snapshot, so one launch over the box computes
+    exactly what the per-region loop of run_target does."""
+    regions = list(bmap.regions)
+    if not regions:
+        return ()
+    nd = len(regions[0].bounds)
+    box = tuple((min(r.bounds[d][0] for r in regions), max(r.bounds[d][1] for r in regions)) for d in range(nd))
+    vol = 1
+    for lo, hi in box:
+        vol *= hi - lo
+    if sum(r.size for r in regions) != vol:
+        raise MatchError("map regions do not form an exact cover of their bounding box")
+    return box
+
+
+def match_map(bmap, *, exact: bool = False) -> MapPlan:
+    """Choose the device kernel for one bound map."""
+    params = dict(bmap.grid_args)  # kernel grid param -> module grid
+    box = map_box(bmap)
+    if exact:
+        p = compile_expr(bmap)
+        p.box, p.reason = box, "precision='exact'"
+        return p
+    try:
+        return _match_fast(bmap, params, box)
+    except MatchError as why:
+        p = compile_expr(bmap)
+        p.box, p.reason = box, str(why)
+        return p
+
+
+def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
+    kern = bmap.kernel
+    if len(kern.updates) != 1:
+        raise MatchError("several updates in one kernel")
+    upd = kern.updates[0]
+    dims = len(upd.offset)
+    if dims != 3:
+        raise MatchError(f"{dims}-D kernel (the streaming kernels are 3-D)")
+    if any(upd.offset):
+        raise MatchError("destination offset is not the centre")
+    scalars = {n: float(v) for n, v in bmap.scalar_args}
+    loc: dict = {}
+    for name, e in kern.locals:
+        loc[name] = expand(e, loc, scalars)
+    expr = upd.expr
+    divisor = 0.0
+    if node_kind(expr) == "Binary" and expr.op == "/" and node_kind(expr.right) == "Const":
+        divisor = float(expr.right.value)  # executor.py:149-153
+        expr = expr.left
+        if divisor == 0.0:
+            raise MatchError("division by zero constant")
+    poly = _drop_zeros(expand(expr, loc, scalars))
+    if () in poly:
+        raise MatchError("constant term")
+    dst = params[upd.dest]
+    deg1 = {k: v for k, v in poly.items() if len(k) == 1}
+    deg2 = {k: v for k, v in poly.items() if len(k) == 2}
+
+    if not deg2:
+        grids = {k[0][0] for k in deg1}
+        if len(grids) != 1:
+            raise MatchError("weighted sum over several grids")
+        src_param = grids.pop()
+        offs = [k[0][1] for k in deg1]
+        if not _is_star(offs, 3):
+            raise MatchError("not star-shaped")
+        r = max(max(abs(c) for c in o) for o in offs)
+        if r < 1 or r > MAX_FAST_RADIUS:
+            raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
+        src = params[src_param]
+        if src == dst:
+            raise MatchError("in-place update (reads and writes the same grid)")
+        coef = [0.0] * (6 * r + 1)
+        for k, v in deg1.items():
+            coef[coef_index(k[0][1], r)] = v
+        return MapPlan("star", r, src, dst, coef=coef, divisor=divisor, box=box)
+
+    if divisor:
+        raise MatchError("divided wave form")
+    # WAVE: deg-2 terms are vel[0] * u[o]
+    vel_cands = None
+    for k in deg2:
+        pair = {k[0], k[1]}
+        zero_reads = {rd for rd in pair if not any(rd[1])}
+        cands = set()
+        for z in zero_reads:
+            other = (pair - {z}) or {z}
+            (o,) = other
+            if o[0] != z[0]:
+                cands.add(z[0])
+        vel_cands = cands if vel_cands is None else (vel_cands & cands)
+    if not vel_cands or len(vel_cands) != 1:
+        raise MatchError("degree-2 terms are not velocity * grid reads")
+    vel_param = vel_cands.pop()
+    u_grids = set()
+    lap = {}
+    for k, v in deg2.items():
+        a, b = k
+        rd = b if (a[0] == vel_param and not any(a[1])) else a
+        u_grids.add(rd[0])
+        lap[rd[1]] = lap.get(rd[1], 0.0) + v
+    if len(u_grids) != 1:
+        raise MatchError("the velocity multiplies reads of several grids")
+    u_param = u_grids.pop()
+    offs = list(lap)
+    if not _is_star(offs, 3):
+        raise MatchError("not star-shaped")
+    r = max(max(abs(c) for c in o) for o in offs)
+    if r < 1 or r > MAX_FAST_RADIUS:
+        raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
+    a_coef, b_coef, prev_param = 0.0, 0.0, None
+    for k, v in deg1.items():
+        (g, o), = k
+        if any(o):
+            raise MatchError("linear term away from the centre")
+        if g == u_param:
+            a_coef += v
+        elif prev_param in (None, g):
+            prev_param, b_coef = g, b_coef + v
+        else:
+            raise MatchError("linear terms over more than two grids")
+    src, vel = params[u_param], params[vel_param]
+    prev = params[prev_param] if prev_param else src
+    if dst in (src, vel):
+        raise MatchError("wave update writes a grid it reads at a non-centre offset")
+    coef = [0.0] * (6 * r + 1)
+    for o, v in lap.items():
+        coef[coef_index(o, r)] = v
+    return MapPlan("wave", r, src, dst, prev=prev, vel=vel, coef=coef, wave_a=a_coef, wave_b=b_coef, box=box)
+
+
+# ---------------------------------------------------------------------------
+# EXPR bytecode
+
+
+def compile_expr(bmap) -> MapPlan:
+    from . import _lib as L
+
+    kern = bmap.kernel
+    gparams = [p for p, _ in bmap.grid_args]
+    index = {p: i for i, p in enumerate(gparams)}
+    if len(gparams) > L.EXPR_MAX_ARGS:
+        raise MatchError(f"kernel has more than {L.EXPR_MAX_ARGS} grid parameters")
+    scalars = {n: float(v) for n, v in bmap.scalar_args}
+    local_ids = {name: i for i, (name, _) in enumerate(kern.locals)}
+    if len(local_ids) > L.EXPR_MAX_LOCALS:
+        raise MatchError("too many kernel locals")
+    code: list = []
+    consts: list = []
+    depth = [0, 0]
+
+    def push(n=1):
+        depth[0] += n
+        depth[1] = max(depth[1], depth[0])
+
+    def const(v: float) -> None:
+        consts.append(float(v))
+        code.append([L.OP_CONST, len(consts) - 1, 0, 0, 0])
+        push()
+
+    def off3(o) -> list:
+        o = list(o)
+        return o + [0] * (3 - len(o))
+
+    def emit(e) -> None:
+        stack = [(e, False)]
+        while stack:  # iterative post-order: deep left-associated sums
+            n, done = stack.pop()
+            k = node_kind(n)
+            if k == "Const":
+                const(n.value)
+            elif k == "Read":
+                if n.grid not in index:
+                    raise MatchError(f"'{n.grid}' is not a grid parameter")
+                code.append([L.OP_READ, index[n.grid], *off3(n.offset)])
+                push()
+            elif k == "Var":
+                if n.name in local_ids:
+                    code.append([L.OP_LOCAL, local_ids[n.name], 0, 0, 0])
+                    push()
+                elif n.name in scalars:
+                    const(scalars[n.name])
+                else:
+                    raise MatchError(f"unbound name '{n.name}' in kernel expression")
+            elif k == "Unary":
+                if done:
+                    code.append([L.OP_NEG, 0, 0, 0, 0])
+                else:
+                    stack.append((n, True))
+                    stack.append((n.operand, False))
+            elif k == "Binary":
+                if done:
+                    op = {"+": L.OP_ADD, "-": L.OP_SUB, "*": L.OP_MUL, "/": L.OP_DIV}[n.op]
+                    code.append([op, 0, 0, 0, 0])
+                    depth[0] -= 1
+                else:
+                    stack.append((n, True))
+                    stack.append((n.right, False))
+                    stack.append((n.left, False))
+            else:
+                raise MatchError(f"unsupported expression node {k}")
+
+    for name, e in kern.locals:
+        emit(e)
+        code.append([L.OP_SETLOCAL, local_ids[name], 0, 0, 0])
+        depth[0] -= 1
+    for upd in kern.updates:
+        emit(upd.expr)
+        code.append([L.OP_STORE, index[upd.dest], *off3(upd.offset)])
+        depth[0] -= 1
+    if depth[1] > L.EXPR_MAX_STACK:
+        raise MatchError("expression nests deeper than the device evaluator's stack")
+    args = [dict(bmap.grid_args)[p] for p in gparams]
+    return MapPlan("expr", args=args, code=code, consts=consts)

@@ -283,13 +283,14 @@ class DeviceTarget:
 
 def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Optional[str] = None,
             args=None, scheme: Optional[str] = None, *, device: Optional[int] = None,
-            precision: str = "fast") -> dict:
+            precision: str = "fast", pinned: bool = False) -> dict:
     """``run_tile_plan`` for GpuPlans, executed on a B200 (executor.py:491-557).
 
     ``precision="fast"`` runs star/wave maps in the grid dtype on the tuned
     streaming kernels (fp32 parity tolerance 1e-5 relative, SURVEY.md §8(c));
     ``precision="exact"`` evaluates every map in float64 in parse order with
-    one rounding per store, bit-identical to ``run_target``.
+    one rounding per store, bit-identical to ``run_target``.  ``pinned=True``
+    returns the device-resident grids in page-locked host memory.
     """
     bound = _prepare(unit, target, args, scheme)
     check_plan(plan, bound)
@@ -301,20 +302,34 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
     for g in used:
         if g not in grids:
             raise ExecutionError(f"grid '{g}' is not among the supplied grids")
-    out = {n: b.copy() for n, b in grids.items()}
     if not used:  # only swaps: exchange identities
+        out = {n: b.copy() for n, b in grids.items()}
         _host_swaps(bound.stmts, out, bindings or {})
         return out
     # grids no map touches still take part in swaps: give them device slots too
     names = used + [n for n in grids if n not in used and _same_layout(grids[n], grids[used[0]])]
+    out = {n: b.copy() for n, b in grids.items() if n not in names}
     with DeviceTarget({n: grids[n] for n in names}, names, device=device, precision=precision) as dt:
         for n in names:
-            dt.upload(n, grids[n].data)
+            dt.upload(n, grids[n].data, sync=False)
+        dt.sync()
         dt.execute(bound.stmts, bindings)
         for n in names:
-            b = out[n]
-            out[n] = type(b)(b.dtype, b.shape, b.order, dt.download(n))
-    return out
+            b = grids[n]
+            arr = _host_array(b.data.shape, dt.np_dtype, pinned)
+            dt.download(n, arr, sync=False)
+            out[n] = type(b)(b.dtype, b.shape, b.order, arr)
+        dt.sync()
+    return {n: out[n] for n in grids}
+
+
+def _host_array(shape, dtype, pinned: bool) -> np.ndarray:
+    if not pinned:
+        return np.empty(shape, dtype=dtype)
+    import torch  # page-locked host memory through torch's caching host allocator
+
+    t = torch.empty(shape, dtype=torch.float32 if dtype == np.float32 else torch.float64, pin_memory=True)
+    return t.numpy()
 
 
 def _same_layout(a, b) -> bool:

@@ -231,3 +231,32 @@ def config_target(kernel: str, shape: Sequence[int], iters, dtype: str = "f32", 
         return jacobi_target(normalised_star_kernel(base), shape, KERNELS[base].radius, iters, dtype,
                              map_width, scheme, f"target_{kernel}")
     return corpus_target(kernel, shape, iters, dtype, map_width=map_width, scheme=scheme)
+
+
+def source_text(kernel: KernelDecl, shape: Sequence[int], order: int, iters: int, dtype: str = "f32",
+                swap: tuple = ("v", "u"), map_width: int = 0, target: str = "",
+                backend: str = "st.seq()") -> str:
+    """A ``.stpy`` program for ``kernel`` in the corpus target shape
+    (corpus.py:127-171): map over the first grid's extent, then swap."""
+    from .program import expr_source
+
+    gparams = [p for p, t in kernel.params if t == "grid"]
+    (upd,) = kernel.updates
+    sig = ", ".join(f"{p}: st.grid" for p in gparams)
+    spec = f"e={gparams[0]}.shape" + (f", w={map_width}" if map_width else "")
+    target = target or "target_" + kernel.name.removeprefix("kernel_")
+    offs = ", ".join(str(c) for c in upd.offset)
+    decls = "".join(
+        f"{p} = st.grid(dtype=st.{dtype}, shape=({', '.join(str(e) for e in shape)}), order={order})\n"
+        for p in gparams)
+    return (
+        "import stencilpy as st\n\n"
+        f"@st.kernel\ndef {kernel.name}({sig}):\n"
+        f"    {upd.dest}.at({offs}).set({expr_source(upd.expr)})\n\n"
+        f"@st.target\ndef {target}({sig}, iter: st.i32):\n"
+        f"    for _t in range(iter):\n"
+        f"        st.map({spec})({kernel.name})({', '.join(gparams)})\n"
+        f"        ({swap[0]}, {swap[1]}) = ({swap[1]}, {swap[0]})\n\n"
+        f"{decls}"
+        f"st.launch(\n    backend={backend}\n)({target})({', '.join(gparams)}, {iters})\n"
+    )

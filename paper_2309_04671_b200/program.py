@@ -323,3 +323,88 @@ def time_loop(name: str, maps: Sequence[BoundMap], swaps: Sequence[tuple], iters
     """``for _t in range(iters): <maps>; (b, a) = (a, b) ...`` as a BoundTarget."""
     body = tuple(maps) + tuple(BoundSwap(a, b) for a, b in swaps)
     return BoundTarget(name, (BoundFor("_t", iters, body),), tuple(grid_params), tuple(scalar_params), scheme)
+
+
+# ---------------------------------------------------------------------------
+# source text and canonical dumps
+
+
+_PREC = {"+": 1, "-": 1, "*": 2, "/": 2}
+
+
+def expr_source(e) -> str:
+    """DSL text whose parse (parser.py:279-321) is exactly the tree ``e``."""
+    k = node_kind(e)
+    if k == "Const":
+        return repr(float(e.value))
+    if k == "Read":
+        return f"{e.grid}.at({', '.join(str(int(c)) for c in e.offset)})"
+    if k == "Var":
+        return e.name
+    if k == "Unary":
+        inner = expr_source(e.operand)
+        return f"-({inner})" if node_kind(e.operand) in ("Binary", "Unary") else f"-{inner}"
+    p = _PREC[e.op]
+    left = expr_source(e.left)
+    if node_kind(e.left) == "Binary" and _PREC[e.left.op] < p:
+        left = f"({left})"
+    right = expr_source(e.right)
+    if node_kind(e.right) == "Binary" and _PREC[e.right.op] <= p:
+        right = f"({right})"
+    elif node_kind(e.right) == "Const" and e.right.value < 0:
+        right = f"({right})"
+    if node_kind(e.left) == "Const" and e.left.value < 0 and p == 2:
+        left = f"({left})"  # (-c) * x parses to Const(-c) either way; keep it explicit
+    return f"{left} {e.op} {right}"
+
+
+def expr_dump(e) -> str:
+    """Fully parenthesised prefix dump, identical for both object models."""
+    out, stack = [], [e]
+    while stack:
+        n = stack.pop()
+        if isinstance(n, str):
+            out.append(n)
+            continue
+        k = node_kind(n)
+        if k == "Const":
+            out.append(repr(float(n.value)))
+        elif k == "Read":
+            out.append(f"{n.grid}{tuple(int(c) for c in n.offset)}")
+        elif k == "Var":
+            out.append(f"${n.name}")
+        elif k == "Unary":
+            stack += [")", n.operand, "(neg "]
+        else:
+            stack += [")", n.right, " ", n.left, f"({n.op} "]
+    return "".join(out)
+
+
+def dump(bound) -> str:
+    """Canonical text of a bound target (statements, maps, kernels, regions)."""
+    lines = [f"target {bound.name} scheme={bound.scheme} grids={tuple(tuple(p) for p in bound.grid_params)}"]
+
+    def rec(stmts, ind):
+        for s in stmts:
+            k = stmt_kind(s)
+            if k == "BoundSwap":
+                lines.append(f"{ind}swap {s.first} {s.second}")
+            elif k == "BoundFor":
+                lines.append(f"{ind}for {s.count}")
+                rec(s.body, ind + "  ")
+            else:
+                kern = s.kernel
+                lines.append(f"{ind}map {kern.name} args={tuple(tuple(a) for a in s.grid_args)} "
+                             f"scalars={tuple(tuple(a) for a in s.scalar_args)}")
+                for name, e in kern.locals:
+                    lines.append(f"{ind}  local {name} = {expr_dump(e)}")
+                for u in kern.updates:
+                    lines.append(f"{ind}  update {u.dest}{tuple(u.offset)} = {expr_dump(u.expr)}")
+                info = s.info
+                lines.append(f"{ind}  info dims={info.dims} radius={info.radius} shape={info.shape} "
+                             f"flops={info.flops_per_point}")
+                for r in s.regions:
+                    lines.append(f"{ind}  region {r.tag} {tuple(tuple(b) for b in r.bounds)}")
+
+    rec(bound.stmts, "  ")
+    return "\n".join(lines) + "\n"

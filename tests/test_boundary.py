@@ -1,0 +1,176 @@
+"""The drop-in boundary, checked without a GPU: the C-ABI library loads and
+exports every entry point include/stkb200.h declares; the matcher routes the
+reference's kernel forms; the device bytecode evaluates (on a CPU emulation
+of its stack machine) to exactly the oracle's results; plans mirror
+planning.py."""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, build_case, golden_cases, load_golden
+from paper_2309_04671_b200 import _lib as L
+from paper_2309_04671_b200 import corpus
+from paper_2309_04671_b200.matcher import coef_index, compile_expr, match_map
+from paper_2309_04671_b200.planning import PlanError, plan_gpu
+
+
+def _maps(stmts):
+    for s in stmts:
+        if type(s).__name__ == "BoundMap":
+            yield s
+        elif type(s).__name__ == "BoundFor":
+            yield from _maps(s.body)
+
+
+def header_symbols():
+    text = (ROOT / "include" / "stkb200.h").read_text()
+    return sorted(set(re.findall(r"\b(stkb_[a-z_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == sorted(L.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    if not L.LIB_PATH.exists():
+        pytest.skip("libstkb200.so not built (run __graft_entry__.build())")
+    lib = L.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.stkb_abi_version() == 1
+
+
+def test_library_rejects_bad_descriptors_without_gpu():
+    if not L.LIB_PATH.exists():
+        pytest.skip("libstkb200.so not built")
+    import ctypes
+
+    lib = L.load()
+    d = L.DomainDesc()
+    d.dtype = 7
+    h = ctypes.c_void_p()
+    assert lib.stkb_domain_create(ctypes.byref(d), ctypes.byref(h)) == L.STKB_ERR_ARG
+    assert b"dtype" in lib.stkb_last_error()
+
+
+@pytest.mark.parametrize("builder,kind", [("star3d4r", "star"), ("star3d1r", "star"), ("star3d2r", "star"),
+                                          ("star3d3r", "star"), ("star3d4r_norm", "star"), ("jacobi7", "star"),
+                                          ("wave", "wave"), ("j3d27pt", "expr"), ("box3d2r", "expr"),
+                                          ("star2d4r", "expr")])
+def test_matcher_routes(builder, kind):
+    shape = (16, 16) if builder.startswith("star2d") else (16, 16, 16)
+    bound, _ = corpus.config_target(builder, shape, 1)
+    plan = match_map(next(_maps(bound.stmts)))
+    assert plan.kind == kind, plan.reason
+
+
+def test_star_coefficients_land_in_abi_slots():
+    bound, _ = corpus.config_target("star3d4r", (16, 16, 16), 1)
+    plan = match_map(next(_maps(bound.stmts)))
+    for off, c in corpus.coefficients(corpus.KERNELS["star3d4r"]):
+        assert plan.coef[coef_index(off, 4)] == c
+    assert plan.divisor == 0.0 and plan.radius == 4
+
+
+def test_normalised_star_keeps_divisor():
+    bound, _ = corpus.config_target("star3d4r_norm", (16, 16, 16), 1)
+    plan = match_map(next(_maps(bound.stmts)))
+    total = round(sum(c for _, c in corpus.coefficients(corpus.KERNELS["star3d4r"])), 5)
+    assert plan.divisor == total
+
+
+def test_wave_form_extracted():
+    bound, _ = corpus.config_target("wave", (16, 16, 16), 1)
+    p = match_map(next(_maps(bound.stmts)))
+    assert (p.src, p.dst, p.prev, p.vel) == ("u", "up", "up", "kap")
+    assert p.wave_a == 2.0 and p.wave_b == -1.0
+    assert p.coef[0] == pytest.approx(3 * corpus.LAP8[0])
+    assert p.coef[coef_index((0, 0, 4), 4)] == pytest.approx(corpus.LAP8[4])
+
+
+def test_in_place_jacobi_goes_exact():
+    from paper_2309_04671_b200.program import BoundMap, KernelDecl, Update
+
+    bound, _ = corpus.config_target("star3d1r", (8, 8, 8), 1)
+    m = next(_maps(bound.stmts))
+    k = m.kernel
+    kk = KernelDecl(k.name, k.params, (), (Update("u", (0, 0, 0), k.updates[0].expr),))
+    p = match_map(BoundMap(kk, m.info, m.grid_args, (), m.spec, m.regions))
+    assert p.kind == "expr" and "in-place" in p.reason
+
+
+def emulate_bytecode(plan, state, bmap):
+    """CPU model of expr_kernel's stack machine, row-vectorised in float64."""
+    code = plan.code
+    box = plan.box if plan.box else None
+    grids = [state[g] for g in plan.args]
+    snaps = [g.data.astype(np.float64) for g in grids]
+    o = grids[0].order
+    nd = len(grids[0].shape)
+    bounds = box
+    ext = tuple(hi - lo for lo, hi in bounds)
+    st, loc = [], {}
+    for op, a, b, c, d in code:
+        off = (b, c, d)[:nd]
+        if op == L.OP_CONST:
+            st.append(np.full(ext, plan.consts[a]))
+        elif op == L.OP_READ:
+            st.append(snaps[a][tuple(slice(o + lo + q, o + hi + q) for (lo, hi), q in zip(bounds, off))])
+        elif op == L.OP_LOCAL:
+            st.append(loc[a])
+        elif op == L.OP_NEG:
+            st.append(-st.pop())
+        elif op == L.OP_SETLOCAL:
+            loc[a] = st.pop()
+        elif op == L.OP_STORE:
+            g = grids[a]
+            g.data[tuple(slice(o + lo + q, o + hi + q) for (lo, hi), q in zip(bounds, off))] = st.pop().astype(g.data.dtype)
+        else:
+            y, x = st.pop(), st.pop()
+            st.append(x + y if op == L.OP_ADD else x - y if op == L.OP_SUB else x * y if op == L.OP_MUL else x / y)
+    assert not st
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_device_bytecode_semantics_bitwise(case):
+    meta, _, _, ins, outs = load_golden(case)
+    bound = build_case(meta)
+    state = {n: b.copy() for n, b in ins.items()}
+
+    def run(stmts):
+        for s in stmts:
+            k = type(s).__name__
+            if k == "BoundSwap":
+                state[s.first], state[s.second] = state[s.second], state[s.first]
+            elif k == "BoundFor":
+                for _ in range(s.count):
+                    run(s.body)
+            else:
+                plan = match_map(s, exact=True)
+                emulate_bytecode(plan, state, s)
+
+    run(bound.stmts)
+    for n, ref in outs.items():
+        assert np.array_equal(state[n].data, ref.data), n
+
+
+def test_plan_gpu_mirrors_reference_rules():
+    bound, _ = corpus.config_target("star3d4r", (16, 16, 16), 1)
+    info = next(_maps(bound.stmts)).info
+    p = plan_gpu(info, {"template": "unroll", "computeCapability": "10.0", "asyncMemcpy": True})
+    assert p.mem_type == "registers" and p.block == (16, 8, 8) and p.plane == (32, 32)
+    assert plan_gpu(info, {"computeCapability": "10.0a"}).compute_capability == "10.0a"
+    with pytest.raises(PlanError, match="unknown GPU template"):
+        plan_gpu(info, {"template": "tma"})
+    with pytest.raises(PlanError, match="asyncMemcpy"):
+        plan_gpu(info, {"asyncMemcpy": True, "computeCapability": "7.5"})
+    with pytest.raises(PlanError, match="unknown GPU parameters"):
+        plan_gpu(info, {"tile": 3})
+    bound, _ = corpus.config_target("star3d4r", (16, 16, 18), 1)
+    with pytest.raises(PlanError, match="divisible by 4"):
+        plan_gpu(next(_maps(bound.stmts)).info, {"template": "f4"})

@@ -55,6 +55,14 @@ def library(entry: dict) -> tuple:
     return REF / entry["lib"], " ".join(entry["cflags"])
 
 
+def _order(builder: str) -> int:
+    if builder == "wave":
+        return 4
+    if builder == "jacobi7":
+        return 1
+    return int(builder.split("d")[1][0])  # star3d<R>r[_norm]
+
+
 def fill(arr: np.ndarray, order: int, seed: int) -> None:
     """Log-uniform interior in [1e-4, 1e5] (grids.py:67-72), drawn plane by plane."""
     rng = np.random.default_rng(seed)
@@ -69,7 +77,7 @@ def run(name: str, steps: int, warmup: int) -> dict:
     lib = ctypes.CDLL(str(path))
     fn = getattr(lib, entry["entry"])
     shape = tuple(entry["shape"])
-    order = {"wave": 4, "jacobi7": 1}.get(entry["builder"], int(entry["builder"].split("d")[1][0]))
+    order = _order(entry["builder"])
     dt = np.float32 if entry["dtype"] == "f32" else np.float64
     cty = ctypes.c_float if entry["dtype"] == "f32" else ctypes.c_double
     padded = tuple(e + 2 * order for e in shape)

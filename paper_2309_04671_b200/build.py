@@ -16,10 +16,12 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libstkb200.so"
-SOURCES = ["star_f32.cu", "star_f64.cu", "expr_kernels.cu", "stkb200.cu"]
+SOURCES = ([f"star_{t}_r{r}.cu" for t in ("f32", "f64") for r in (1, 2, 3, 4)]
+           + ["star_dispatch.cu", "expr_kernels.cu", "stkb200.cu"])
 HEADERS = ["common.cuh", "star_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"),
+         f"-DSTKB_VARIANTS={int(os.environ.get('STKB_BUILD_VARIANTS', '1'))}"]
 
 
 def nvcc() -> str:
@@ -40,6 +42,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "stkb200.h"]
     jobs = []
+    stamp = OBJ / "flags.txt"
+    flags_txt = " ".join(FLAGS)
+    if not stamp.exists() or stamp.read_text() != flags_txt:
+        force = True
     for src in SOURCES:
         obj = OBJ / (Path(src).stem + ".o")
         if force or _stale(obj, [CSRC / src, *hdrs]):
@@ -55,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
+    stamp.write_text(flags_txt)
     objs = [OBJ / (Path(s).stem + ".o") for s in SOURCES]
     if force or jobs or _stale(LIB, objs):
         run([nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *map(str, objs), "-o", str(LIB)])

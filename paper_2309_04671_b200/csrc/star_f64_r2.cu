@@ -1,0 +1,8 @@
+// f64 radius-2 instantiations of the streaming star kernels (one TU per radius: parallel builds).
+#include "star_kernels.cuh"
+
+namespace stkb {
+cudaError_t launch_star_f64_r2(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s) {
+    return launch_star_r<double, 2>(L, a, L.maps, s);
+}
+}  // namespace stkb

@@ -23,6 +23,8 @@
 //    stage as extra TMA centre boxes, so the epilogue never waits on HBM.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace stkb {
@@ -53,15 +55,73 @@ struct StarCfg {
     static_assert(SW <= 256 && SH <= 256, "TMA box dims are limited to 256");
 };
 
-template <typename T>
-__device__ __forceinline__ void lds16(const T* p, T* v) {
-    using V = typename Vec16<T>::type;
-    V t = *reinterpret_cast<const V*>(p);
-    if constexpr (sizeof(T) == 4) { v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
-    else { v[0] = t.x; v[1] = t.y; }
+// 128-bit shared loads through an explicit shared-window address (LDS.128;
+// a generic pointer here would compile to LD.E.128 through the generic path)
+__device__ __forceinline__ void lds16(const float* p, float* v) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void lds16(const double* p, double* v) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(smem_u32(p)));
 }
 
-template <typename T, int R, int FORM, int TY, int NWY>
+// ---------------------------------------------------------------------------
+// lane packs: fp32 runs two points per instruction (FFMA2 / FMUL2, sm_100),
+// fp64 one.  `Pk<T>::P` holds W consecutive d2 points of one row.
+template <typename T> struct Pk;
+template <> struct Pk<float> {
+    static constexpr int W = 2;
+    struct P { float x, y; };
+    static __device__ __forceinline__ P make(const float* v) { return P{v[0], v[1]}; }
+    static __device__ __forceinline__ void put(float* v, P p) { v[0] = p.x; v[1] = p.y; }
+    static __device__ __forceinline__ P fma(float c, P b, P acc) {  // c*b + acc, c broadcast
+        P d;
+        asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+            "mov.b64 rc, {%5, %6};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+            : "=f"(d.x), "=f"(d.y) : "f"(c), "f"(b.x), "f"(b.y), "f"(acc.x), "f"(acc.y));
+        return d;
+    }
+    static __device__ __forceinline__ P fmav(P a, P b, P acc) {  // a*b + acc, lane-wise
+        P d;
+        asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+            "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+            : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(acc.x), "f"(acc.y));
+        return d;
+    }
+    static __device__ __forceinline__ P mul(float c, P b) {
+        P d;
+        asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+            "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+            : "=f"(d.x), "=f"(d.y) : "f"(c), "f"(b.x), "f"(b.y));
+        return d;
+    }
+    // 0 stays 0 for finite lanes; an inf/nan lane turns the check into nan
+    static __device__ __forceinline__ P check(P v, P chk) { return fma(0.0f, v, chk); }
+    static __device__ __forceinline__ bool clean(P chk) { return chk.x == 0.0f && chk.y == 0.0f; }
+};
+template <> struct Pk<double> {
+    static constexpr int W = 1;
+    struct P { double x; };
+    static __device__ __forceinline__ P make(const double* v) { return P{v[0]}; }
+    static __device__ __forceinline__ void put(double* v, P p) { v[0] = p.x; }
+    static __device__ __forceinline__ P fma(double c, P b, P acc) { return P{__fma_rn(c, b.x, acc.x)}; }
+    static __device__ __forceinline__ P fmav(P a, P b, P acc) { return P{__fma_rn(a.x, b.x, acc.x)}; }
+    static __device__ __forceinline__ P mul(double c, P b) { return P{__dmul_rn(c, b.x)}; }
+    static __device__ __forceinline__ P check(P v, P chk) { return P{__fma_rn(0.0, v.x, chk.x)}; }
+    static __device__ __forceinline__ bool clean(P chk) { return chk.x == 0.0; }
+};
+
+// cold path: one output row of a tile that straddles the region box
+template <typename T>
+__device__ __noinline__ void store_row_masked(T* dz, T v0, T v1, T v2, T v3, int x, int lo2, int hi2) {
+    constexpr int VEC = 16 / sizeof(T);
+    const T v[4] = {v0, v1, v2, v3};
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+        if (x + i >= lo2 && x + i < hi2) dz[i] = v[i];
+}
+
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
 __global__ void __launch_bounds__((NWY + 1) * 32, 1)
 star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_ctr,
@@ -143,17 +203,22 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     }
 
     // ---------------------------------------------------------------- consumers
-    const int xl = lane * VEC;  // d2 offset inside the tile
-    const int jr0 = warp * TY;  // first d1 row of this warp inside the tile
-    T acc[NS][TY][VEC];
+    using K = Pk<T>;
+    using P = typename K::P;
+    constexpr int W = K::W;
+    constexpr int NPK = VEC / W;  // lane packs per 16-byte row vector
+    const int xl = lane * VEC;    // d2 offset inside the tile
+    const int jr0 = warp * TY;    // first d1 row of this warp inside the tile
+    P acc[NS][TY][NPK];
 #pragma unroll
     for (int k = 0; k < NS; ++k)
 #pragma unroll
         for (int j = 0; j < TY; ++j)
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) acc[k][j][i] = T(0);
-    bool bad = false;
+            for (int i = 0; i < NPK; ++i) acc[k][j][i] = K::mul(T(0), P{});
+    P chk = K::mul(T(0), P{});
     uint32_t it = 0;
+    const int64_t pitch = a.g.pitch, plane = a.g.plane;
 
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const int tx = item % a.n_tx;
@@ -166,8 +231,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         const int z1 = min(z0 + a.lz, a.box.hi0);
         const int x = x0 + xl;
         const int nq = (z1 - z0) + 2 * R;
+        const bool full_tile = x0 >= a.box.lo2 && x0 + BX <= a.box.hi2 && y0 >= a.box.lo1 && y0 + BY <= a.box.hi1;
         const bool x_full = (x >= a.box.lo2) && (x + VEC <= a.box.hi2);
         const bool x_any = (x + VEC > a.box.lo2) && (x < a.box.hi2);
+        // output address of row jr0 at plane z: dst0 + (z + order0) * plane + j * pitch
+        T* const dst0 = a.dst + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x;
 
         for (int qb = 0; qb < nq; qb += NS) {
 #pragma unroll
@@ -181,17 +249,20 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     const T* t = tiles + size_t(s) * C::STAGE_ELEMS;
 
                     // centre values of this thread's rows in plane q
-                    T cv[TY][VEC];
+                    T cvs[TY][VEC];
 #pragma unroll
-                    for (int j = 0; j < TY; ++j) lds16(t + (jr0 + j + R) * SW + xl + RA, cv[j]);
+                    for (int j = 0; j < TY; ++j) lds16(t + (jr0 + j + R) * SW + xl + RA, cvs[j]);
+                    P cv[TY][NPK];
+#pragma unroll
+                    for (int j = 0; j < TY; ++j)
+#pragma unroll
+                        for (int k = 0; k < NPK; ++k) cv[j][k] = K::make(&cvs[j][k * W]);
 
-                    const bool main_plane = (q >= z0) && (q < z1);
-                    if (main_plane) {
-                        T ip[TY][VEC];
-                        // d2 (x) taps: left/right vectors of each centre row
+                    if (q >= z0 && q < z1) {
+                        // output q: its accumulator already holds the d0 taps of planes < q
 #pragma unroll
                         for (int j = 0; j < TY; ++j) {
-                            T xr[VEC + 2 * RA];
+                            T xr[VEC + 2 * RA];  // left halo | centre | right halo of row j
                             const T* row = t + (jr0 + j + R) * SW + xl;
 #pragma unroll
                             for (int k = 0; k < RA / VEC; ++k) {
@@ -199,123 +270,122 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                 lds16(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
                             }
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) xr[RA + i] = cv[j][i];
+                            for (int i = 0; i < VEC; ++i) xr[RA + i] = cvs[j][i];
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                T s_ = a.c0 * cv[j][i];
+                            for (int k = 0; k < NPK; ++k) {
+                                P s_ = K::fma(a.c0, cv[j][k], acc[p][j][k]);
 #pragma unroll
                                 for (int m = 1; m <= R; ++m) {
-                                    s_ = fma_t(a.cm[2][m - 1], xr[RA + i - m], s_);
-                                    s_ = fma_t(a.cp[2][m - 1], xr[RA + i + m], s_);
+                                    if (W == 1 || (m % 2) == 0 || !ODD_SCALAR) {
+                                        s_ = K::fma(a.cm[2][m - 1], K::make(&xr[RA + k * W - m]), s_);
+                                        s_ = K::fma(a.cp[2][m - 1], K::make(&xr[RA + k * W + m]), s_);
+                                    } else {  // odd shift: the pair straddles two register pairs
+                                        T l[W], r[W];
+                                        K::put(l, s_);
+#pragma unroll
+                                        for (int w = 0; w < W; ++w) {
+                                            l[w] = fma_t(a.cm[2][m - 1], xr[RA + k * W + w - m], l[w]);
+                                            l[w] = fma_t(a.cp[2][m - 1], xr[RA + k * W + w + m], l[w]);
+                                        }
+                                        (void)r;
+                                        s_ = K::make(l);
+                                    }
                                 }
-                                ip[j][i] = s_;
+                                acc[p][j][k] = s_;
                             }
                         }
                         // d1 (y) taps: stream the TY+2R rows of this warp's column
 #pragma unroll
                         for (int rr = 0; rr < TY + 2 * R; ++rr) {
-                            T yv[VEC];
                             if (rr >= R && rr < R + TY) {
 #pragma unroll
-                                for (int i = 0; i < VEC; ++i) yv[i] = cv[rr - R][i];
-                            } else {
-                                lds16(t + (jr0 + rr) * SW + xl + RA, yv);
-                            }
-#pragma unroll
-                            for (int j = 0; j < TY; ++j) {
-                                const int m = rr - (j + R);
-                                if (m != 0 && m >= -R && m <= R) {
-#pragma unroll
-                                    for (int i = 0; i < VEC; ++i) {
+                                for (int j = 0; j < TY; ++j) {
+                                    const int m = rr - (j + R);
+                                    if (m != 0 && m >= -R && m <= R) {
                                         const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
-                                        ip[j][i] = fma_t(c, yv[i], ip[j][i]);
+#pragma unroll
+                                        for (int k = 0; k < NPK; ++k)
+                                            acc[p][j][k] = K::fma(c, cv[rr - R][k], acc[p][j][k]);
+                                    }
+                                }
+                            } else {
+                                T yv[VEC];
+                                lds16(t + (jr0 + rr) * SW + xl + RA, yv);
+#pragma unroll
+                                for (int j = 0; j < TY; ++j) {
+                                    const int m = rr - (j + R);
+                                    if (m >= -R && m <= R) {
+                                        const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
+#pragma unroll
+                                        for (int k = 0; k < NPK; ++k)
+                                            acc[p][j][k] = K::fma(c, K::make(&yv[k * W]), acc[p][j][k]);
                                     }
                                 }
                             }
                         }
-                        // output q: its accumulator already holds the d0 taps of planes < q
-#pragma unroll
-                        for (int j = 0; j < TY; ++j)
-#pragma unroll
-                            for (int i = 0; i < VEC; ++i) acc[p][j][i] += ip[j][i];
                     }
                     if (q < z1) {
                         // plane q feeds future outputs q+m with the -m coefficient
 #pragma unroll
                         for (int j = 0; j < TY; ++j)
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                acc[(p + R) % NS][j][i] = a.cm[0][R - 1] * cv[j][i];
+                            for (int k = 0; k < NPK; ++k) {
+                                acc[(p + R) % NS][j][k] = K::mul(a.cm[0][R - 1], cv[j][k]);
 #pragma unroll
                                 for (int m = 1; m < R; ++m)
-                                    acc[(p + m) % NS][j][i] =
-                                        fma_t(a.cm[0][m - 1], cv[j][i], acc[(p + m) % NS][j][i]);
+                                    acc[(p + m) % NS][j][k] = K::fma(a.cm[0][m - 1], cv[j][k], acc[(p + m) % NS][j][k]);
                             }
                     }
                     // plane q feeds past outputs q-m with the +m coefficient
 #pragma unroll
                     for (int j = 0; j < TY; ++j)
 #pragma unroll
-                        for (int i = 0; i < VEC; ++i)
+                        for (int k = 0; k < NPK; ++k)
 #pragma unroll
                             for (int m = 1; m <= R; ++m)
-                                acc[(p - m + NS) % NS][j][i] =
-                                    fma_t(a.cp[0][m - 1], cv[j][i], acc[(p - m + NS) % NS][j][i]);
+                                acc[(p - m + NS) % NS][j][k] =
+                                    K::fma(a.cp[0][m - 1], cv[j][k], acc[(p - m + NS) % NS][j][k]);
 
                     // output plane z = q - R is complete
                     const int z = q - R;
                     const bool z_out = (z >= z0) && (z < z1);
-                    constexpr int ks = (NS - R) % NS;  // slot offset of q - R relative to p
+                    constexpr int ks = (NS - R) % NS;  // slot of output q - R relative to p
                     T outv[TY][VEC];
                     if (z_out) {
 #pragma unroll
                         for (int j = 0; j < TY; ++j)
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) {
-                                T v = acc[(p + ks) % NS][j][i];
-                                if constexpr (FORM == FORM_STAR_DIV) v = v / a.divisor;
-                                outv[j][i] = v;
+                            for (int k = 0; k < NPK; ++k) {
+                                P v = acc[(p + ks) % NS][j][k];
+                                if constexpr (FORM == FORM_STAR_DIV) v = K::mul(a.divisor, v);  // host passes 1/divisor
+                                if constexpr (FORM == FORM_WAVE) {
+                                    const T* cu = t + C::HALO_ELEMS + (jr0 + j) * BX + xl + k * W;
+                                    const P uu = K::make(cu);
+                                    const P pp = K::make(cu + C::CTR_ELEMS);
+                                    const P kk = K::make(cu + 2 * C::CTR_ELEMS);
+                                    v = K::fmav(kk, v, K::fma(a.wave_b, pp, K::mul(a.wave_a, uu)));
+                                }
+                                K::put(&outv[j][k * W], v);
+                                chk = K::check(v, chk);
                             }
-                        if constexpr (FORM == FORM_WAVE) {
-                            const T* cu = t + C::HALO_ELEMS;
-                            const T* cpv = cu + C::CTR_ELEMS;
-                            const T* cvl = cpv + C::CTR_ELEMS;
-#pragma unroll
-                            for (int j = 0; j < TY; ++j) {
-                                T uu[VEC], pp[VEC], kk[VEC];
-                                const int o = (jr0 + j) * BX + xl;
-                                lds16(cu + o, uu);
-                                lds16(cpv + o, pp);
-                                lds16(cvl + o, kk);
-#pragma unroll
-                                for (int i = 0; i < VEC; ++i)
-                                    outv[j][i] = fma_t(kk[i], outv[j][i], fma_t(a.wave_b, pp[i], a.wave_a * uu[i]));
-                            }
-                        }
                     }
                     // every shared read of stage s is done: hand it back to the producer
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                     ++it;
 
-                    if (z_out && x_any) {
+                    if (z_out) {
+                        T* const dz = dst0 + (int64_t(z) + a.g.order0) * plane;
+                        if (full_tile) {
 #pragma unroll
-                        for (int j = 0; j < TY; ++j) {
-                            const int y = y0 + jr0 + j;
-                            if (y >= a.box.lo1 && y < a.box.hi1) {
-                                T* dp = a.dst + a.g.at(z, y, x);
-                                if (x_full) {
-                                    stg16(dp, outv[j]);
+                            for (int j = 0; j < TY; ++j) stg16(dz + j * pitch, outv[j]);
+                        } else if (x_any) {
 #pragma unroll
-                                    for (int i = 0; i < VEC; ++i) bad |= !isfinite(outv[j][i]);
-                                } else {
-#pragma unroll
-                                    for (int i = 0; i < VEC; ++i)
-                                        if (x + i >= a.box.lo2 && x + i < a.box.hi2) {
-                                            dp[i] = outv[j][i];
-                                            bad |= !isfinite(outv[j][i]);
-                                        }
-                                }
+                            for (int j = 0; j < TY; ++j) {
+                                const int y = y0 + jr0 + j;
+                                if (y >= a.box.lo1 && y < a.box.hi1)
+                                    store_row_masked<T>(dz + j * pitch, outv[j][0], outv[j][1 % VEC],
+                                                        outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2, a.box.hi2);
                             }
                         }
                     }
@@ -323,7 +393,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
             }
         }
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
+    if (__any_sync(0xffffffffu, !K::clean(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
 // pick the z-chunk length: minimise the per-CTA critical path in plane steps
@@ -344,12 +414,10 @@ inline int choose_lz(int n0, int tiles, int ctas, int R, int* n_tz) {
     return best;
 }
 
-template <typename T, int R, int FORM, int TY>
-cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps,
-                            cudaStream_t stream) {
-    constexpr int NWY = 7;  // 7 consumer warps + 1 TMA producer warp: 2 warps per SMSP -> 255 regs/thread
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
+cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps, cudaStream_t stream) {
     using C = StarCfg<T, R, FORM, TY, NWY>;
-    auto kern = star_stream_kernel<T, R, FORM, TY, NWY>;
+    auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -375,23 +443,56 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     return cudaGetLastError();
 }
 
+// tile variants: (rows per warp, consumer warps, odd x-taps as scalar FMAs)
+struct Variant { int ty, nwy; bool odd_scalar; };
+
 template <typename T>
-constexpr int star_ty(int R) {
-    return sizeof(T) == 4 ? (R == 1 ? 8 : (R == 2 ? 6 : 4)) : (R == 1 ? 8 : 4);
+__host__ __device__ constexpr Variant star_variant_of(int R, int v) {
+    if (sizeof(T) == 8) return Variant{R == 1 ? 8 : 4, 7, true};
+    switch (v) {
+        case 1: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, true};   // wide rows, 1 warp pair / SMSP
+        case 2: return Variant{R == 1 ? 6 : 3, 10, true};
+        case 3: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, false};  // odd x-taps as re-paired FFMA2
+        default: return Variant{R == 1 ? 4 : 2, 15, true};                 // measured best on B200 (tools/sweep.py)
+    }
 }
+
+inline int star_variant_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("STKB_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <typename T, int R, int V>
+cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
+    constexpr Variant vv = star_variant_of<T>(R, V);
+    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+    if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+    return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+}
+
+#ifndef STKB_VARIANTS
+#define STKB_VARIANTS 1
+#endif
 
 template <typename T, int R>
-cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps,
-                          cudaStream_t s) {
-    constexpr int TY = star_ty<T>(R);
-    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, TY>(L, a, maps, s);
-    if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, TY>(L, a, maps, s);
-    return launch_star_cfg<T, R, FORM_STAR, TY>(L, a, maps, s);
+cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4 && STKB_VARIANTS > 1) {
+        switch (star_variant_env()) {
+            case 1: return launch_star_v<T, R, 1>(L, a, maps, s);
+            case 2: return launch_star_v<T, R, 2>(L, a, maps, s);
+            case 3: return launch_star_v<T, R, 3>(L, a, maps, s);
+            default: break;
+        }
+    }
+    return launch_star_v<T, R, 0>(L, a, maps, s);
 }
 
 template <typename T>
-cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps,
-                          cudaStream_t s) {
+cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
     switch (L.radius) {
         case 1: return launch_star_r<T, 1>(L, a, maps, s);
         case 2: return launch_star_r<T, 2>(L, a, maps, s);
@@ -405,9 +506,10 @@ cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUten
 template <typename T>
 inline void star_tile_t(int R, int* bx, int* by, int* halo_x) {
     constexpr int VEC = 16 / sizeof(T);
-    const int ty = R == 1 ? star_ty<T>(1) : R == 2 ? star_ty<T>(2) : R == 3 ? star_ty<T>(3) : star_ty<T>(4);
+    const int v = (sizeof(T) == 4 && STKB_VARIANTS > 1) ? star_variant_env() : 0;
+    const Variant vv = star_variant_of<T>(R, v);
     *bx = 32 * VEC;
-    *by = 7 * ty;
+    *by = vv.nwy * vv.ty;
     *halo_x = ((R + VEC - 1) / VEC) * VEC;
 }
 

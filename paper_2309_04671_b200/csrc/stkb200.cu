@@ -162,7 +162,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
             a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)]) : T(0);
             a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1]) : T(0);
         }
-    a.divisor = T(d.divisor);
+    a.divisor = d.divisor != 0.0 ? T(1.0 / d.divisor) : T(0);  // the kernel multiplies by the reciprocal
     a.wave_a = T(d.wave_a);
     a.wave_b = T(d.wave_b);
 

@@ -42,11 +42,13 @@ struct StarArgs {
     const T* prev;             // WAVE
     const T* vel;              // WAVE
     int32_t* nonfinite;        // sticky flag
+    int32_t* work_counter;     // dynamic tile scheduler (reset before each launch)
     T c0;                      // centre
     T cm[3][4];                // [axis][m-1] coefficient of offset -m
     T cp[3][4];                // [axis][m-1] coefficient of offset +m
     T divisor;
     T wave_a, wave_b;
+    int32_t store_hint;        // 1: streaming (evict-first) output stores
 };
 
 // ---------------------------------------------------------------------------
@@ -132,6 +134,12 @@ __device__ __forceinline__ void ldg16(const T* p, T (&v)[16 / sizeof(T)]) {
         double2 t = __ldg(reinterpret_cast<const double2*>(p));
         v[0] = t.x; v[1] = t.y;
     }
+}
+
+template <typename T>
+__device__ __forceinline__ void stg16_cs(T* p, const T (&v)[16 / sizeof(T)]) {
+    if constexpr (sizeof(T) == 4) __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+    else __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
 }
 
 template <typename T>

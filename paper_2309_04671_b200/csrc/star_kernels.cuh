@@ -49,7 +49,8 @@ struct StarCfg {
     static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * sizeof(T);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-    static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+    static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
+                                   STAGES * sizeof(int32_t);
     static constexpr int THREADS = (NWY + 1) * 32;
     static_assert(STAGE_BYTES % 128 == 0, "stage must keep 128-B alignment");
     static_assert(SW <= 256 && SH <= 256, "TMA box dims are limited to 256");
@@ -139,6 +140,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     T* tiles = reinterpret_cast<T*>(base);
     uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(STAGES) * C::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
+    volatile int32_t* stage_item = reinterpret_cast<int32_t*>(empty + STAGES);  // work item of each stage
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -163,7 +165,18 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 prefetch_tmap(&tm_vel);
             }
             uint32_t it = 0;
-            for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+            // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
+            // order, so CTAs working at the same time stream neighbouring tiles and
+            // share their halo rows through L2
+            while (true) {
+                const int item = atomicAdd(a.work_counter, 1);
+                if (item >= a.n_items) {
+                    const uint32_t s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                    stage_item[s] = -1;  // sentinel: no more work
+                    mbar_arrive(&full[s]);
+                    break;
+                }
                 const int tx = item % a.n_tx;
                 const int rest = item / a.n_tx;
                 const int ty = rest % a.n_ty;
@@ -178,6 +191,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     const uint32_t s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
+                    stage_item[s] = item;
                     T* st = tiles + size_t(s) * C::STAGE_ELEMS;
                     if constexpr (FORM == FORM_WAVE) {
                         const int z = q - R;  // output plane completed at this step
@@ -220,7 +234,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     uint32_t it = 0;
     const int64_t pitch = a.g.pitch, plane = a.g.plane;
 
-    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+    while (true) {
+        // the producer tags every stage with its work item; -1 ends the kernel
+        mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
+        const int item = stage_item[it % STAGES];
+        if (item < 0) break;
         const int tx = item % a.n_tx;
         const int rest = item / a.n_tx;
         const int ty = rest % a.n_ty;
@@ -377,8 +395,13 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     if (z_out) {
                         T* const dz = dst0 + (int64_t(z) + a.g.order0) * plane;
                         if (full_tile) {
+                            if (a.store_hint) {
 #pragma unroll
-                            for (int j = 0; j < TY; ++j) stg16(dz + j * pitch, outv[j]);
+                                for (int j = 0; j < TY; ++j) stg16_cs(dz + j * pitch, outv[j]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < TY; ++j) stg16(dz + j * pitch, outv[j]);
+                            }
                         } else if (x_any) {
 #pragma unroll
                             for (int j = 0; j < TY; ++j) {
@@ -396,19 +419,21 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     if (__any_sync(0xffffffffu, !K::clean(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
-// pick the z-chunk length: minimise the per-CTA critical path in plane steps
+// pick the z-chunk length for the dynamic scheduler: the mean per-CTA work in
+// plane steps (every chunk re-streams 2R halo planes) plus one item of tail
 inline int choose_lz(int n0, int tiles, int ctas, int R, int* n_tz) {
-    long best_cost = -1;
+    double best_cost = -1.0;
     int best = n0;
-    for (int lz = 1; lz <= n0; ++lz) {
-        const int tz = (n0 + lz - 1) / lz;
-        const long items = long(tiles) * tz;
-        const long waves = (items + ctas - 1) / ctas;
-        const long cost = waves * (lz + 2 * R);
-        if (best_cost < 0 || cost < best_cost || (cost == best_cost && lz > best)) {
+    for (int lz = 8; lz <= n0 + 7; lz += 8) {
+        const int l = lz < n0 ? lz : n0;
+        const int tz = (n0 + l - 1) / l;
+        const double planes = double(tiles) * (n0 + 2.0 * R * tz);
+        const double cost = planes / ctas + 1.0 * (l + 2 * R) + (tiles * tz < ctas ? 1e9 / (tiles * tz) : 0.0);
+        if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
-            best = lz;
+            best = l;
         }
+        if (l == n0) break;
     }
     *n_tz = (n0 + best - 1) / best;
     return best;
@@ -439,6 +464,8 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     a.n_items = tiles * a.n_tz;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;
+    cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
     kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], a);
     return cudaGetLastError();
 }

@@ -48,9 +48,11 @@ int fail(int code, const std::string& msg) {
     } while (0)
 
 constexpr int kMaxTags = 64;
+constexpr int kMaxMaps = 256;
 
 struct MapOp {
     stkb_map_desc d;
+    int slot = 0;  // index of this map's scheduler counter
     std::vector<int32_t> code;
     std::vector<double> consts;
     int32_t* d_code = nullptr;
@@ -104,6 +106,8 @@ struct stkb_domain {
     void* d_partials = nullptr;
     int lz_override = 0;
     int ctas_override = 0;
+    int l2promo = 3;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
+    int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
 };
 
 namespace {
@@ -123,9 +127,11 @@ int encode_map(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap**
     cuuint64_t strides[2] = {cuuint64_t(g.pitch * dom->elem), cuuint64_t(g.plane * dom->elem)};
     cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(bh), 1};
     cuuint32_t estr[3] = {1, 1, 1};
+    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
     CUresult r = g_encode(&m, dom->elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                           3, dom->bufs[buffer], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promo[dom->l2promo & 3],
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     auto res = dom->tmaps.emplace(key, m);
@@ -155,6 +161,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.prev = d.prev >= 0 ? static_cast<const T*>(dom->bufs[bind[d.prev]]) : nullptr;
     a.vel = d.vel >= 0 ? static_cast<const T*>(dom->bufs[bind[d.vel]]) : nullptr;
     a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
+    a.work_counter = dom->d_flags + kMaxTags + op.slot;
     const int R = d.radius;
     a.c0 = T(d.coef[0]);
     for (int ax = 0; ax < 3; ++ax)
@@ -165,6 +172,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.divisor = d.divisor != 0.0 ? T(1.0 / d.divisor) : T(0);  // the kernel multiplies by the reciprocal
     a.wave_a = T(d.wave_a);
     a.wave_b = T(d.wave_b);
+    a.store_hint = dom->store_hint;
 
     int bx, by, hx;
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
@@ -323,10 +331,13 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (cudaStreamCreateWithFlags(&dom->own_stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup("stream");
     dom->stream = dom->own_stream;
     if (cudaEventCreate(&dom->ev0) != cudaSuccess || cudaEventCreate(&dom->ev1) != cudaSuccess) return cleanup("event");
-    if (cudaMalloc(&dom->d_flags, kMaxTags * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
-    cudaMemset(dom->d_flags, 0, kMaxTags * sizeof(int32_t));
+    // [0, kMaxTags): sticky non-finite flags per map tag; then one scheduler counter per map
+    if (cudaMalloc(&dom->d_flags, (kMaxTags + kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
+    cudaMemset(dom->d_flags, 0, (kMaxTags + kMaxMaps) * sizeof(int32_t));
     if (const char* s = getenv("STKB_LZ")) dom->lz_override = atoi(s);
     if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
+    if (const char* s = getenv("STKB_L2PROMO")) dom->l2promo = atoi(s);
+    if (const char* s = getenv("STKB_STORE_HINT")) dom->store_hint = atoi(s);
     *out = dom;
     return STKB_OK;
 }
@@ -535,6 +546,8 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     } else {
         return fail(STKB_ERR_ARG, "unknown map kind");
     }
+    if (dom->maps.size() >= size_t(kMaxMaps)) return fail(STKB_ERR_ARG, "too many maps in one step program");
+    op.slot = int(dom->maps.size());
     invalidate_graph(dom);
     dom->maps.push_back(std::move(op));
     dom->prog.push_back(ProgOp{0, int(dom->maps.size()) - 1, 0, 0});

@@ -142,6 +142,16 @@ int stkb_launches(stkb_domain *dom, int64_t *count); /* kernels launched by the 
 int stkb_binding(const stkb_domain *dom, int32_t name, int32_t *buffer);
 int stkb_nonfinite(stkb_domain *dom, int32_t tag, int32_t *flag); /* sticky; clears it */
 
+/* Fine-grained control for the multi-GPU z-slab driver: launch program map
+ * `map_index` restricted to interior d0 planes [lo0, hi0) on the domain's
+ * current stream; apply a name swap now; address a contiguous run of d0
+ * planes (interior index z0, may be negative for halo planes) of the buffer a
+ * name is bound to, for halo exchange over NCCL / peer memory. */
+int stkb_launch_map(stkb_domain *dom, int32_t map_index, int64_t lo0, int64_t hi0);
+int stkb_apply_swap(stkb_domain *dom, int32_t a, int32_t b);
+int stkb_plane_span(stkb_domain *dom, int32_t name, int64_t z0, int64_t nplanes, void **dptr,
+                    int64_t *bytes);
+
 /* Compatibility entry with the reference C-ABI's semantics (serial.py:126-208):
  * upload every grid, run the program `iters` times, download every grid under
  * its final name, synchronously.  host[i] is GridBuffer.data of name i. */

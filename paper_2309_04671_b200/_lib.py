@@ -32,7 +32,7 @@ EXPORTS = (
     "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_program_reset",
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
-    "stkb_compare",
+    "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span",
 )
 
 
@@ -120,6 +120,9 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_nonfinite": [V, i32, P(i32)],
         "stkb_run_target": [V, P(V), i64],
         "stkb_compare": [V, i32, i32, P(dbl), P(dbl), P(i64), P(dbl)],
+        "stkb_launch_map": [V, i32, i64, i64],
+        "stkb_apply_swap": [V, i32, i32],
+        "stkb_plane_span": [V, i32, i64, i64, P(V), P(i64)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -666,6 +666,43 @@ int stkb_nonfinite(stkb_domain* dom, int32_t tag, int32_t* flag) {
     return STKB_OK;
 }
 
+int stkb_launch_map(stkb_domain* dom, int32_t map_index, int64_t lo0, int64_t hi0) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    MapOp& op = dom->maps[map_index];
+    const stkb_map_desc saved = op.d;
+    op.d.lo[0] = std::max<int64_t>(saved.lo[0], lo0);
+    op.d.hi[0] = std::min<int64_t>(saved.hi[0], hi0);
+    int rc = STKB_OK;
+    if (op.d.hi[0] > op.d.lo[0]) {
+        if (op.d.kind == STKB_MAP_EXPR) rc = launch_expr_map(dom, op, dom->binding);
+        else if (dom->desc.dtype == STKB_F32) rc = launch_star_map<float>(dom, op, dom->binding);
+        else rc = launch_star_map<double>(dom, op, dom->binding);
+    }
+    op.d = saved;
+    return rc;
+}
+
+int stkb_apply_swap(stkb_domain* dom, int32_t a, int32_t b) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (int rc = check_name(dom, a, "swap")) return rc;
+    if (int rc = check_name(dom, b, "swap")) return rc;
+    std::swap(dom->binding[a], dom->binding[b]);
+    return STKB_OK;
+}
+
+int stkb_plane_span(stkb_domain* dom, int32_t name, int64_t z0, int64_t nplanes, void** dptr, int64_t* bytes) {
+    if (!dom || !dptr || !bytes) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_plane_span")) return rc;
+    const Geometry& g = dom->g;
+    if (nplanes < 0 || z0 < -g.order0 || z0 + nplanes > g.n0 + g.order0)
+        return fail(STKB_ERR_ARG, "plane span outside the padded grid");
+    *dptr = static_cast<char*>(dom->bufs[dom->binding[name]]) + size_t(z0 + g.order0) * size_t(g.plane) * dom->elem;
+    *bytes = nplanes * g.plane * int64_t(dom->elem);
+    return STKB_OK;
+}
+
 int stkb_run_target(stkb_domain* dom, void* const* host, int64_t iters) {
     if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
     for (int i = 0; i < dom->desc.n_grids; ++i)

@@ -1,0 +1,326 @@
+"""Multi-GPU z-slab decomposition with halo exchange.
+
+One process per GPU.  The streaming axis d0 is cut into contiguous slabs, one
+per rank; rank r stores its ``n_r`` interior planes plus the grid's ``order``
+halo planes on each side, so its d0 halo holds the neighbour's boundary
+planes (or, at the two ends, the global frozen zero halo, grids.py:22-27).
+After a map writes a grid whose values are read at a non-zero d0 offset in
+the next step, the R boundary planes go to each neighbour's halo (R = the
+largest |d0 offset| read).  With a pitched layout every d0 plane is one
+contiguous block, so each message is one contiguous buffer.
+
+Per step and per exchanged map (north star): the two boundary sub-slabs
+[0, R) and [n-R, n) are computed first; the NCCL send/recv of those planes
+runs on a side stream while the interior [R, n-R) computes; the compute
+stream then joins the exchange before the next map reads the halo.
+
+The schedule and message layout (:class:`SlabPlan`) are device-independent:
+the CPU tests drive them with ``gloo`` and the oracle, the GPU path with NCCL
+and the sm_100a kernels (:class:`DeviceSlabEngine`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .program import node_kind, stmt_kind, walk
+
+
+def partition(n0: int, world: int) -> list:
+    """Contiguous d0 slabs [(start, size)] as even as possible (larger first)."""
+    if world < 1 or n0 < world:
+        raise ValueError(f"cannot cut {n0} planes into {world} slabs")
+    base, extra = divmod(n0, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((z, n))
+        z += n
+    return out
+
+
+def d0_read_reach(bmap) -> dict:
+    """{module grid: max |d0 offset| read by this map}."""
+    params = dict(bmap.grid_args)
+    reach: dict = {}
+    kern = bmap.kernel
+    for e in [e for _, e in kern.locals] + [u.expr for u in kern.updates]:
+        for n in walk(e):
+            if node_kind(n) == "Read":
+                g = params[n.grid]
+                reach[g] = max(reach.get(g, 0), abs(int(n.offset[0])))
+    return reach
+
+
+def written(bmap) -> list:
+    params = dict(bmap.grid_args)
+    return [params[u.dest] for u in bmap.kernel.updates]
+
+
+def exchange_schedule(body: tuple) -> list:
+    """Per statement of the step body: {name: R} to exchange after it.
+
+    A map's destination is exchanged when the *buffer* it wrote is read at a
+    non-zero d0 offset before it is written again, following name swaps
+    through two consecutive steps (the body repeats)."""
+    names = sorted({g for s in body if stmt_kind(s) == "BoundMap" for _, g in s.grid_args}
+                   | {x for s in body if stmt_kind(s) == "BoundSwap" for x in (s.first, s.second)})
+    sched = [dict() for _ in body]
+    for i, s in enumerate(body):
+        if stmt_kind(s) != "BoundMap":
+            continue
+        for dname in written(s):
+            bind = {n: n for n in names}  # name -> buffer identity at step start
+            # replay statements up to i to learn which buffer dname denotes
+            for t in body[:i]:
+                if stmt_kind(t) == "BoundSwap":
+                    bind[t.first], bind[t.second] = bind[t.second], bind[t.first]
+            buf = bind[dname]
+            need = 0
+            seq = list(body[i + 1:]) + list(body)  # rest of this step, then the next one
+            for t in seq:
+                k = stmt_kind(t)
+                if k == "BoundSwap":
+                    bind[t.first], bind[t.second] = bind[t.second], bind[t.first]
+                    continue
+                reach = d0_read_reach(t)
+                inv = {b: n for n, b in bind.items()}
+                rn = inv.get(buf)
+                if rn is not None and reach.get(rn, 0) > 0:
+                    need = max(need, reach[rn])
+                if rn is not None and rn in written(t):
+                    break
+            if need:
+                sched[i][dname] = need
+    return sched
+
+
+@dataclass
+class SlabPlan:
+    """Rank-local geometry and messages of one slab decomposition."""
+
+    n0: int
+    world: int
+    rank: int
+    order: int
+
+    def __post_init__(self):
+        self.parts = partition(self.n0, self.world)
+        self.start, self.size = self.parts[self.rank]
+        if self.world > 1 and min(n for _, n in self.parts) < self.order:
+            raise ValueError(f"slabs of {min(n for _, n in self.parts)} planes are thinner than the halo ({self.order})")
+
+    @property
+    def lower(self) -> Optional[int]:
+        return self.rank - 1 if self.rank > 0 else None
+
+    @property
+    def upper(self) -> Optional[int]:
+        return self.rank + 1 if self.rank < self.world - 1 else None
+
+    def messages(self, reach: int) -> list:
+        """[(op, peer, local first interior plane index, planes)] for one grid:
+        my R lowest planes go down (land in the lower rank's top halo), my R top
+        planes go up; I receive into my own halo planes."""
+        out = []
+        if self.lower is not None:
+            out.append(("send", self.lower, 0, reach))
+            out.append(("recv", self.lower, -reach, reach))
+        if self.upper is not None:
+            out.append(("send", self.upper, self.size - reach, reach))
+            out.append(("recv", self.upper, self.size, reach))
+        return out
+
+    def global_slice(self) -> slice:
+        """Padded-d0 slice of a global GridBuffer.data this rank holds (halo included)."""
+        return slice(self.start, self.start + self.size + 2 * self.order)
+
+
+def exchange(dist, plan: SlabPlan, views: dict, group=None):
+    """Post all sends/recvs of one exchange as one batch; returns the work handles.
+
+    ``views[(grid, first_plane, planes)]`` -> contiguous tensor."""
+    ops = []
+    for grid, reach in views["_reach"].items():
+        for op, peer, z, n in plan.messages(reach):
+            t = views[(grid, z, n)]
+            fn = dist.isend if op == "send" else dist.irecv
+            ops.append(dist.P2POp(fn, t, peer, group))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+def run_step(eng, dist, group=None) -> None:
+    """One time step of ``eng.body`` on this rank's slab.
+
+    ``eng`` provides launch(i, lo0, hi0), swap(a, b), view(grid, z0, planes),
+    and the overlap hooks boundary_done() / comm_context(token) / join(works);
+    the device engine maps them to CUDA streams, the CPU test engine to no-ops."""
+    plan = eng.plan
+    n = plan.size
+    for i, s in enumerate(eng.body):
+        if stmt_kind(s) == "BoundSwap":
+            eng.swap(s.first, s.second)
+            continue
+        ex = eng.sched[i]
+        if not ex or plan.world == 1:
+            eng.launch(i, 0, n)
+            continue
+        r = max(ex.values())
+        # boundary planes first, then the exchange overlaps the interior
+        eng.launch(i, 0, min(r, n))
+        eng.launch(i, max(n - r, r), n)
+        token = eng.boundary_done()
+        views = {"_reach": ex}
+        for g, reach in ex.items():
+            for _, _, z, m in plan.messages(reach):
+                views[(g, z, m)] = eng.view(g, z, m)
+        with eng.comm_context(token):
+            works = exchange(dist, plan, views, group)
+        eng.launch(i, r, n - r)
+        eng.join(works)
+
+
+class DeviceSlabEngine:
+    """The rank-local slab on this GPU: a DeviceTarget driven map by map."""
+
+    def __init__(self, body: tuple, decls: dict, plan: SlabPlan, device: int, precision: str = "fast"):
+        import torch
+
+        from .backend import DeviceTarget
+        from .grids import GridBuffer
+
+        self.torch = torch
+        self.plan = plan
+        self.body = tuple(body)
+        self.sched = exchange_schedule(self.body)
+        names = list(decls)
+        d0 = next(iter(decls.values()))
+        local_shape = (plan.size,) + tuple(d0.shape[1:])
+        stub = {n: GridBuffer(decls[n].dtype, local_shape, decls[n].order, np.zeros((1,) * 3, np.float32))
+                for n in names}
+        self.dt = DeviceTarget(stub, names, device=device, precision=precision)
+        self.dt.set_program(self.body)
+        self.map_index = {}
+        k = 0
+        for i, s in enumerate(self.body):
+            if stmt_kind(s) == "BoundMap":
+                self.map_index[i] = k
+                k += 1
+        self.compute = torch.cuda.Stream(device=device)
+        self.comm = torch.cuda.Stream(device=device)
+        self.dt.set_stream(self.compute.cuda_stream)
+        self.tdtype = torch.float32 if d0.dtype == "f32" else torch.float64
+        self.launches = 0
+
+    def view(self, name: str, z0: int, n: int):
+        from . import _lib as L
+
+        p, b = ctypes.c_void_p(), ctypes.c_int64()
+        L.call("stkb_plane_span", self.dt.h, self.dt.index[name], z0, n, ctypes.byref(p), ctypes.byref(b))
+        nelem = b.value // (4 if self.tdtype == self.torch.float32 else 8)
+        typestr = "<f4" if self.tdtype == self.torch.float32 else "<f8"
+
+        class _A:
+            __cuda_array_interface__ = {"shape": (nelem,), "typestr": typestr, "data": (p.value, False),
+                                        "version": 2}
+
+        return self.torch.as_tensor(_A(), device=f"cuda:{self.dt.device}")
+
+    def launch(self, i: int, lo0: int, hi0: int) -> None:
+        from . import _lib as L
+
+        if hi0 > lo0:
+            L.call("stkb_launch_map", self.dt.h, self.map_index[i], lo0, hi0)
+            self.launches += 1
+
+    def swap(self, a: str, b: str) -> None:
+        from . import _lib as L
+
+        L.call("stkb_apply_swap", self.dt.h, self.dt.index[a], self.dt.index[b])
+
+    def boundary_done(self):
+        ev = self.torch.cuda.Event()
+        ev.record(self.compute)
+        return ev
+
+    def comm_context(self, ev):
+        self.comm.wait_event(ev)
+        return self.torch.cuda.stream(self.comm)
+
+    def join(self, works) -> None:
+        with self.torch.cuda.stream(self.compute):
+            for w in works:
+                w.wait()
+        self.compute.wait_stream(self.comm)
+
+    def step(self, dist, group=None) -> None:
+        run_step(self, dist, group)
+
+    def close(self):
+        self.dt.close()
+
+
+class SlabBench:
+    """bench.py's N>1 path: strong scaling of one configuration over z-slabs."""
+
+    def __init__(self, builder: str, shape, dtype: str, world: int, rank: int, device: int):
+        import torch
+        import torch.distributed as dist
+
+        from . import corpus
+
+        self.dist = dist
+        bound, decls = corpus.config_target(builder, shape, 1, dtype)
+        body = next(s for s in bound.stmts if stmt_kind(s) == "BoundFor").body
+        order = next(iter(decls.values())).order
+        self.plan = SlabPlan(shape[0], world, rank, order)
+        self.eng = DeviceSlabEngine(body, decls, self.plan, device)
+        self.local_points = self.plan.size * int(np.prod(shape[1:]))
+        self.kind = self.eng.dt.plans[0].kind
+        self._fill(builder, decls)
+        self.torch = torch
+
+    def _fill(self, builder, decls):
+        import bench  # the synthetic device fill lives with the benchmark
+
+        names = list(decls)
+        shp = (self.plan.size,) + tuple(next(iter(decls.values())).shape[1:])
+        bench.fill_device(self.eng.dt, names, shp, builder, seed=7 + self.plan.rank)
+
+    def warmup(self, w: int) -> None:
+        for _ in range(w):
+            self.eng.step(self.dist)
+        self.torch.cuda.synchronize()
+        self.dist.barrier()
+
+    def timed(self, k: int):
+        torch = self.torch
+        self.dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.eng.launches = 0
+        s.record(self.eng.compute)
+        for _ in range(k):
+            self.eng.step(self.dist)
+        e.record(self.eng.compute)
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        return s.elapsed_time(e), self.eng.launches
+
+    def comm_info(self) -> dict:
+        ex = [x for x in self.eng.sched if x]
+        lay = self.eng.dt.layout()
+        esz = 4 if self.eng.tdtype == self.torch.float32 else 8
+        r = max((max(x.values()) for x in ex), default=0)
+        return {"backend": "nccl send/recv (batch_isend_irecv) on a side stream, overlapped with the interior",
+                "planes_per_message": r, "bytes_per_message": r * lay["plane"] * esz,
+                "slab_planes": self.plan.size}
+
+    def close(self):
+        self.eng.close()

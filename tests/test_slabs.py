@@ -1,0 +1,140 @@
+"""Multi-GPU z-slab logic on CPU (gloo, world_size 2 and 3).
+
+The slab plan, exchange schedule, message layout and the boundary-first /
+overlap / join step order (paper_2309_04671_b200.slabs.run_step) are the
+same code the GPU path runs; here the per-rank "kernel" is the oracle over
+the rank's sub-box and the transport is gloo.  The gathered result must be
+bit-identical to the unsplit oracle (SURVEY.md §8(e) test).
+"""
+
+from __future__ import annotations
+
+import contextlib
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle
+from paper_2309_04671_b200 import corpus
+from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
+from paper_2309_04671_b200.slabs import SlabPlan, exchange_schedule, partition, run_step
+
+
+def test_partition_even_and_ragged():
+    assert partition(1024, 8) == [(128 * r, 128) for r in range(8)]
+    assert partition(10, 3) == [(0, 4), (4, 3), (7, 3)]
+    with pytest.raises(ValueError):
+        partition(2, 3)
+
+
+def test_exchange_schedule_forms():
+    for builder, dst, r in (("star3d4r", "v", 4), ("star3d1r", "v", 1), ("wave", "up", 4), ("jacobi7", "v", 1)):
+        bound, _ = corpus.config_target(builder, (16, 16, 16), 1)
+        body = bound.stmts[0].body
+        sched = exchange_schedule(body)
+        assert sched[0] == {dst: r}, builder
+        assert sched[1] == {}
+
+
+def test_messages_land_in_neighbour_halo():
+    mid = SlabPlan(30, 3, 1, 4)
+    assert mid.messages(4) == [("send", 0, 0, 4), ("recv", 0, -4, 4), ("send", 2, 6, 4), ("recv", 2, 10, 4)]
+    assert SlabPlan(30, 3, 0, 4).messages(2) == [("send", 1, 8, 2), ("recv", 1, 10, 2)]
+
+
+class CpuSlabEngine:
+    """Oracle-backed stand-in for DeviceSlabEngine (same run_step driver)."""
+
+    def __init__(self, body, local: dict, plan: SlabPlan):
+        self.body, self.state, self.plan = tuple(body), local, plan
+        self.sched = exchange_schedule(self.body)
+
+    def launch(self, i, lo0, hi0):
+        if hi0 <= lo0:
+            return
+        bmap = self.body[i]
+        m = oracle._Map(bmap, self.state)
+        for reg in bmap.regions:
+            b = list(reg.bounds)
+            b[0] = (max(b[0][0], lo0), min(b[0][1], hi0))
+            m.region(tuple(b))
+
+    def swap(self, a, b):
+        self.state[a], self.state[b] = self.state[b], self.state[a]
+
+    def view(self, g, z0, n):
+        buf = self.state[g]
+        o = buf.order
+        flat = torch.from_numpy(buf.data.reshape(-1))
+        per = int(np.prod(buf.data.shape[1:]))
+        return flat[(z0 + o) * per:(z0 + o + n) * per]
+
+    def boundary_done(self):
+        return None
+
+    def comm_context(self, _):
+        return contextlib.nullcontext()
+
+    def join(self, works):
+        for w in works:
+            w.wait()
+
+
+def _global_case(builder, shape, steps):
+    bound, decls = corpus.config_target(builder, shape, steps)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    if builder == "wave":
+        corpus.wave_inputs(grids)
+    else:
+        fill_loguniform(grids["u"], 5)
+    return bound, grids
+
+
+def _worker(rank, world, port, builder, shape, steps, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bound, grids = _global_case(builder, shape, steps)
+        order = next(iter(grids.values())).order
+        plan = SlabPlan(shape[0], world, rank, order)
+        local = {}
+        for n, g in grids.items():
+            data = np.ascontiguousarray(g.data[plan.global_slice()])
+            local[n] = GridBuffer(g.dtype, (plan.size,) + tuple(shape[1:]), order, data)
+        eng = CpuSlabEngine(bound.stmts[0].body, local, plan)
+        for _ in range(steps):
+            run_step(eng, dist)
+        for n, g in eng.state.items():
+            np.save(os.path.join(outdir, f"{n}_{rank}.npy"), g.interior)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,builder,shape,steps", [
+    (2, "star3d4r_norm", (20, 12, 16), 4),
+    (3, "star3d2r", (17, 9, 12), 3),
+    (2, "wave", (18, 10, 12), 5),
+    (3, "jacobi7", (10, 8, 8), 6),
+])
+def test_slab_run_bitwise_equals_unsplit_oracle(world, builder, shape, steps):
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker, args=(world, _free_port(), builder, shape, steps, d), nprocs=world,
+                           join=True, start_method="spawn")
+        bound, grids = _global_case(builder, shape, steps)
+        ref = oracle.run_target(bound, grids)
+        for n, g in ref.items():
+            parts = [np.load(os.path.join(d, f"{n}_{r}.npy")) for r in range(world)]
+            assert np.array_equal(np.concatenate(parts, axis=0), g.interior), n

@@ -155,6 +155,26 @@ def exchange(dist, plan: SlabPlan, views: dict, group=None):
     return dist.batch_isend_irecv(ops)
 
 
+def localize(body: tuple, start: int, size: int) -> tuple:
+    """The step body as seen by the slab [start, start+size): every map's
+    regions are clipped to the slab and shifted to local d0 coordinates."""
+    from .program import BoundMap, Region
+
+    out = []
+    for s in body:
+        if stmt_kind(s) != "BoundMap":
+            out.append(s)
+            continue
+        regs = []
+        for r in s.regions:
+            (lo, hi), rest = r.bounds[0], tuple(r.bounds[1:])
+            lo, hi = max(lo, start), min(hi, start + size)
+            if hi > lo:
+                regs.append(Region(((lo - start, hi - start),) + rest, r.tag))
+        out.append(BoundMap(s.kernel, s.info, tuple(s.grid_args), tuple(s.scalar_args), s.spec, tuple(regs)))
+    return tuple(out)
+
+
 def run_step(eng, dist, group=None) -> None:
     """One time step of ``eng.body`` on this rank's slab.
 
@@ -205,7 +225,8 @@ class DeviceSlabEngine:
         stub = {n: GridBuffer(decls[n].dtype, local_shape, decls[n].order, np.zeros((1,) * 3, np.float32))
                 for n in names}
         self.dt = DeviceTarget(stub, names, device=device, precision=precision)
-        self.dt.set_program(self.body)
+        self.local_body = localize(self.body, plan.start, plan.size)
+        self.dt.set_program(self.local_body)
         self.map_index = {}
         k = 0
         for i, s in enumerate(self.body):

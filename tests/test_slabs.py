@@ -23,7 +23,7 @@ import torch.multiprocessing as mp
 from oracle import oracle
 from paper_2309_04671_b200 import corpus
 from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
-from paper_2309_04671_b200.slabs import SlabPlan, exchange_schedule, partition, run_step
+from paper_2309_04671_b200.slabs import SlabPlan, exchange_schedule, localize, partition, run_step
 
 
 def test_partition_even_and_ragged():
@@ -54,11 +54,12 @@ class CpuSlabEngine:
     def __init__(self, body, local: dict, plan: SlabPlan):
         self.body, self.state, self.plan = tuple(body), local, plan
         self.sched = exchange_schedule(self.body)
+        self.local_body = localize(self.body, plan.start, plan.size)
 
     def launch(self, i, lo0, hi0):
         if hi0 <= lo0:
             return
-        bmap = self.body[i]
+        bmap = self.local_body[i]
         m = oracle._Map(bmap, self.state)
         for reg in bmap.regions:
             b = list(reg.bounds)
@@ -86,8 +87,8 @@ class CpuSlabEngine:
             w.wait()
 
 
-def _global_case(builder, shape, steps):
-    bound, decls = corpus.config_target(builder, shape, steps)
+def _global_case(builder, shape, steps, width=0):
+    bound, decls = corpus.config_target(builder, shape, steps, map_width=width)
     grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
     if builder == "wave":
         corpus.wave_inputs(grids)
@@ -96,12 +97,12 @@ def _global_case(builder, shape, steps):
     return bound, grids
 
 
-def _worker(rank, world, port, builder, shape, steps, outdir):
+def _worker(rank, world, port, builder, shape, steps, outdir, width):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        bound, grids = _global_case(builder, shape, steps)
+        bound, grids = _global_case(builder, shape, steps, width)
         order = next(iter(grids.values())).order
         plan = SlabPlan(shape[0], world, rank, order)
         local = {}
@@ -123,17 +124,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,builder,shape,steps", [
-    (2, "star3d4r_norm", (20, 12, 16), 4),
-    (3, "star3d2r", (17, 9, 12), 3),
-    (2, "wave", (18, 10, 12), 5),
-    (3, "jacobi7", (10, 8, 8), 6),
+@pytest.mark.parametrize("world,builder,shape,steps,width", [
+    (2, "star3d4r_norm", (20, 12, 16), 4, 0),
+    (3, "star3d2r", (17, 9, 12), 3, 0),
+    (2, "wave", (18, 10, 12), 5, 0),
+    (3, "jacobi7", (10, 8, 8), 6, 0),
+    (2, "star3d4r_norm", (22, 14, 12), 3, 3),  # PML-style regions clipped per slab
 ])
-def test_slab_run_bitwise_equals_unsplit_oracle(world, builder, shape, steps):
+def test_slab_run_bitwise_equals_unsplit_oracle(world, builder, shape, steps, width):
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(_worker, args=(world, _free_port(), builder, shape, steps, d), nprocs=world,
+        mp.start_processes(_worker, args=(world, _free_port(), builder, shape, steps, d, width), nprocs=world,
                            join=True, start_method="spawn")
-        bound, grids = _global_case(builder, shape, steps)
+        bound, grids = _global_case(builder, shape, steps, width)
         ref = oracle.run_target(bound, grids)
         for n, g in ref.items():
             parts = [np.load(os.path.join(d, f"{n}_{r}.npy")) for r in range(world)]

@@ -43,6 +43,16 @@ CONFIGS = {
 METRIC = "25-pt star fp32 GPts/s at 1/2/4/8 B200; achieved HBM GB/s vs peak"
 
 
+def ncu_traffic(config: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text()).get(config)
+        if d:
+            return float(d["bytes"]) / 1e9, d["source"]
+    return None, None
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -265,6 +275,7 @@ def run_ours(args) -> None:
             cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {exc}"[:300]}
 
+    traffic_gb, traffic_src = ncu_traffic(args.config) if ws == 1 else (None, None)
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -286,7 +297,11 @@ def run_ours(args) -> None:
                        "l2": "no flush needed: each grid (4.6 GB) >> L2 (126 MB)",
                        "timing": "CUDA events on the kernel stream around K graph-replayed steps; max over ranks"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": round(achieved / peaks["hbm"], 4), "traffic": args.traffic,
+                         "frac": round(achieved / peaks["hbm"], 4),
+                         "traffic": args.traffic if args.traffic is not None else traffic_gb,
+                         "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                         "traffic_source": traffic_src,
+                         "algorithmic_gb_per_launch": round(local_pts * bpp / 1e9, 4),
                          "peak_source": peaks["src"],
                          "algorithmic_bytes_per_point": bpp,
                          "per_launch": f"{local_pts} points x {bpp} B / mean step time (one kernel per step)"},

@@ -88,7 +88,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("STKB_LIB", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build the CUDA backend first (python -m paper_2309_04671_b200.build "

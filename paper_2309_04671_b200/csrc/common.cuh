@@ -24,6 +24,8 @@ struct Geometry {
     }
 };
 
+constexpr int kMaxChunks = 96;
+
 struct Box {
     int32_t lo0, hi0, lo1, hi1, lo2, hi2;
 };
@@ -35,7 +37,8 @@ struct StarArgs {
     Box box;
     int32_t x0base;            // lo2 rounded down to the vector width
     int32_t n_tx, n_ty, n_tz;  // work-item grid: x tiles, y tiles, z chunks
-    int32_t lz;                // z-chunk length
+    int32_t lz;                // nominal z-chunk length (chunk bounds in zc)
+    int32_t zc[kMaxChunks + 1];  // z-chunk boundaries relative to box.lo0 (tapered at the end)
     int32_t n_items;
     T* dst;
     const T* src;              // centre re-read (WAVE)
@@ -166,6 +169,7 @@ struct StarLaunch {
     int num_sms;
     int max_ctas;      // 0 = auto (one per SM)
     int lz;            // 0 = auto
+    bool taper;        // shorten the last z-chunks
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);

@@ -183,8 +183,8 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 const int tz = rest / a.n_ty;
                 const int x0 = a.x0base + tx * BX;
                 const int y0 = a.box.lo1 + ty * BY;
-                const int z0 = a.box.lo0 + tz * a.lz;
-                const int z1 = min(z0 + a.lz, a.box.hi0);
+                const int z0 = a.box.lo0 + a.zc[tz];
+                const int z1 = a.box.lo0 + a.zc[tz + 1];
                 const int c0 = int(a.g.lead) + x0 - RA;
                 const int c1 = y0 + int(a.g.order) - R;
                 for (int q = z0 - R; q < z1 + R; ++q, ++it) {
@@ -245,8 +245,8 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         const int tz = rest / a.n_ty;
         const int x0 = a.x0base + tx * BX;
         const int y0 = a.box.lo1 + ty * BY;
-        const int z0 = a.box.lo0 + tz * a.lz;
-        const int z1 = min(z0 + a.lz, a.box.hi0);
+        const int z0 = a.box.lo0 + a.zc[tz];
+        const int z1 = a.box.lo0 + a.zc[tz + 1];
         const int x = x0 + xl;
         const int nq = (z1 - z0) + 2 * R;
         const bool full_tile = x0 >= a.box.lo2 && x0 + BX <= a.box.hi2 && y0 >= a.box.lo1 && y0 + BY <= a.box.hi1;
@@ -276,7 +276,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
 #pragma unroll
                         for (int k = 0; k < NPK; ++k) cv[j][k] = K::make(&cvs[j][k * W]);
 
+#ifdef STKB_EXP_NOBRANCH
+                    if (true) {
+#else
                     if (q >= z0 && q < z1) {
+#endif
                         // output q: its accumulator already holds the d0 taps of planes < q
 #pragma unroll
                         for (int j = 0; j < TY; ++j) {
@@ -312,6 +316,35 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                 acc[p][j][k] = s_;
                             }
                         }
+#ifdef STKB_EXP_YSPLIT
+                        // d1 (y) taps into a second accumulator chain (shorter FMA dependency chains)
+                        P yacc[TY][NPK];
+#pragma unroll
+                        for (int rr = 0; rr < TY + 2 * R; ++rr) {
+                            T yv[VEC];
+                            if (rr >= R && rr < R + TY) {
+#pragma unroll
+                                for (int i = 0; i < VEC; ++i) yv[i] = cvs[rr - R][i];
+                            } else {
+                                lds16(t + (jr0 + rr) * SW + xl + RA, yv);
+                            }
+#pragma unroll
+                            for (int j = 0; j < TY; ++j) {
+                                const int m = rr - (j + R);
+                                if (m != 0 && m >= -R && m <= R) {
+                                    const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
+#pragma unroll
+                                    for (int k = 0; k < NPK; ++k)
+                                        yacc[j][k] = (m == -R) ? K::mul(c, K::make(&yv[k * W]))
+                                                               : K::fma(c, K::make(&yv[k * W]), yacc[j][k]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < TY; ++j)
+#pragma unroll
+                            for (int k = 0; k < NPK; ++k) acc[p][j][k] = K::fma(T(1), yacc[j][k], acc[p][j][k]);
+#else
                         // d1 (y) taps: stream the TY+2R rows of this warp's column
 #pragma unroll
                         for (int rr = 0; rr < TY + 2 * R; ++rr) {
@@ -341,8 +374,13 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                 }
                             }
                         }
+#endif
                     }
+#ifdef STKB_EXP_NOBRANCH
+                    if (true) {
+#else
                     if (q < z1) {
+#endif
                         // plane q feeds future outputs q+m with the -m coefficient
 #pragma unroll
                         for (int j = 0; j < TY; ++j)
@@ -366,7 +404,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
 
                     // output plane z = q - R is complete
                     const int z = q - R;
+#ifdef STKB_EXP_NOBRANCH
+                    const bool z_out = (z >= z0);
+#else
                     const bool z_out = (z >= z0) && (z < z1);
+#endif
                     constexpr int ks = (NS - R) % NS;  // slot of output q - R relative to p
                     T outv[TY][VEC];
                     if (z_out) {
@@ -439,6 +481,33 @@ inline int choose_lz(int n0, int tiles, int ctas, int R, int* n_tz) {
     return best;
 }
 
+// z-chunk boundaries: uniform chunks of `lz`, except that the last chunks halve
+// (lz/2, lz/4, ... >= 16) so the scheduler's final round is short (smaller tail)
+inline void chunk_bounds(int n0, int lz, int tiles, int ctas, bool taper, int32_t* zc, int32_t* n_tz) {
+    int tail[16], nt = 0, tail_sum = 0;
+    if (taper && 2 * tiles >= ctas)
+        for (int l = lz / 2; l >= 16 && nt < 16; l /= 2) {
+            tail[nt++] = l;
+            tail_sum += l;
+        }
+    int main_len = n0 - tail_sum;
+    if (main_len < lz) {  // too short to taper
+        nt = 0;
+        main_len = n0;
+    }
+    int k = 0;
+    zc[k++] = 0;
+    const int n_main = (main_len + lz - 1) / lz;
+    for (int c = 1; c <= n_main && k <= kMaxChunks; ++c) zc[k++] = int32_t((int64_t(main_len) * c) / n_main);
+    int z = main_len;
+    for (int i = 0; i < nt && k <= kMaxChunks; ++i) {
+        z += tail[i];
+        zc[k++] = z;
+    }
+    zc[k - 1] = n0;
+    *n_tz = k - 1;
+}
+
 template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
 cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps, cudaStream_t stream) {
     using C = StarCfg<T, R, FORM, TY, NWY>;
@@ -461,6 +530,12 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     } else {
         a.lz = choose_lz(n0, tiles, ctas, R, &a.n_tz);
     }
+    if (a.n_tz > kMaxChunks) {
+        a.n_tz = kMaxChunks;
+        a.lz = (n0 + kMaxChunks - 1) / kMaxChunks;
+        a.n_tz = (n0 + a.lz - 1) / a.lz;
+    }
+    chunk_bounds(n0, a.lz, tiles, ctas, L.taper, a.zc, &a.n_tz);
     a.n_items = tiles * a.n_tz;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;

@@ -108,6 +108,7 @@ struct stkb_domain {
     int ctas_override = 0;
     int l2promo = 3;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
+    bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
 };
 
 namespace {
@@ -199,6 +200,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.num_sms = dom->num_sms;
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;
+    L.taper = dom->taper;
     cudaError_t e;
     if constexpr (sizeof(T) == 4) e = launch_star_f32(L, a, dom->stream);
     else e = launch_star_f64(L, a, dom->stream);
@@ -338,6 +340,7 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
     if (const char* s = getenv("STKB_L2PROMO")) dom->l2promo = atoi(s);
     if (const char* s = getenv("STKB_STORE_HINT")) dom->store_hint = atoi(s);
+    if (const char* s = getenv("STKB_TAPER")) dom->taper = atoi(s) != 0;
     *out = dom;
     return STKB_OK;
 }

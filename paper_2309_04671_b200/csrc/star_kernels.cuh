@@ -550,7 +550,7 @@ struct Variant { int ty, nwy; bool odd_scalar; };
 
 template <typename T>
 __host__ __device__ constexpr Variant star_variant_of(int R, int v) {
-    if (sizeof(T) == 8) return Variant{R == 1 ? 8 : 4, 7, true};
+    if (sizeof(T) == 8 && v == 9) return Variant{R == 1 ? 8 : 4, 7, true};  // previous fp64 default
     switch (v) {
         case 1: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, true};   // wide rows, 1 warp pair / SMSP
         case 2: return Variant{R == 1 ? 6 : 3, 10, true};
@@ -582,7 +582,7 @@ cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUten
 
 template <typename T, int R>
 cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
-    if constexpr (sizeof(T) == 4 && STKB_VARIANTS > 1) {
+    if constexpr (STKB_VARIANTS > 1) {
         switch (star_variant_env()) {
             case 1: return launch_star_v<T, R, 1>(L, a, maps, s);
             case 2: return launch_star_v<T, R, 2>(L, a, maps, s);
@@ -608,7 +608,7 @@ cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUten
 template <typename T>
 inline void star_tile_t(int R, int* bx, int* by, int* halo_x) {
     constexpr int VEC = 16 / sizeof(T);
-    const int v = (sizeof(T) == 4 && STKB_VARIANTS > 1) ? star_variant_env() : 0;
+    const int v = STKB_VARIANTS > 1 ? star_variant_env() : 0;
     const Variant vv = star_variant_of<T>(R, v);
     *bx = 32 * VEC;
     *by = vv.nwy * vv.ty;

@@ -46,6 +46,8 @@ extern "C" {
 /* map kinds */
 #define STKB_MAP_STAR 1 /* dst = (sum_k c_k * src[o_k]) [/ divisor], star offsets, radius <= 4 */
 #define STKB_MAP_WAVE 2 /* dst = a*src[0] + b*prev[0] + vel[0] * (sum_k c_k * src[o_k]) */
+#define STKB_MAP_BOX 4  /* dst = (sum over the dense (2R+1)^3 cube c[dz][dy][dx] * src[o]) [/ divisor],
+                           R <= 2: box, j3d27pt-style and "other" shapes inside the cube */
 #define STKB_MAP_EXPR 3 /* any kernel: bytecode evaluated in float64, parse order,
                            one rounding per store (bit-identical to run_target,
                            executor.py:267-286) */
@@ -86,7 +88,7 @@ typedef struct {
 
 typedef struct {
     int32_t kind;      /* STKB_MAP_* */
-    int32_t radius;    /* STAR/WAVE: star radius 1..4 */
+    int32_t radius;    /* STAR/WAVE: star radius 1..4; BOX: 1..2 */
     int32_t src;       /* STAR/WAVE: name read at the star offsets */
     int32_t dst;       /* STAR/WAVE: name written at offset 0 */
     int32_t prev;      /* WAVE: name read at offset 0 (may equal dst: in-place) */
@@ -109,6 +111,8 @@ typedef struct {
     const int32_t *code;
     int32_t n_consts;
     const double *consts;
+    /* BOX only: box_coef[((dz+R)*(2R+1) + (dy+R))*(2R+1) + (dx+R)] */
+    double box_coef[125];
 } stkb_map_desc;
 
 /* library */

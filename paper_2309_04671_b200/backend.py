@@ -184,15 +184,18 @@ class DeviceTarget:
         bx = box if box is not None else plan.box
         for i, (lo, hi) in enumerate(bx):
             d.lo[i], d.hi[i] = lo, hi
-        if plan.kind in ("star", "wave"):
-            d.kind = L.STKB_MAP_STAR if plan.kind == "star" else L.STKB_MAP_WAVE
+        if plan.kind in ("star", "wave", "box"):
+            d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX}[plan.kind]
             d.radius = plan.radius
             d.src, d.dst = self.index[plan.src], self.index[plan.dst]
             if plan.kind == "wave":
                 d.prev, d.vel = self.index[plan.prev], self.index[plan.vel]
                 d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
             for i, c in enumerate(plan.coef):
-                d.coef[i] = c
+                if plan.kind == "box":
+                    d.box_coef[i] = c
+                else:
+                    d.coef[i] = c
             d.divisor = plan.divisor
         else:
             d.kind = L.STKB_MAP_EXPR

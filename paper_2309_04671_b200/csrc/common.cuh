@@ -51,6 +51,7 @@ struct StarArgs {
     T cp[3][4];                // [axis][m-1] coefficient of offset +m
     T divisor;
     T wave_a, wave_b;
+    T cb[125];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 2
     int32_t store_hint;        // 1: streaming (evict-first) output stores
 };
 
@@ -162,7 +163,7 @@ __device__ __forceinline__ double fma_t(double a, double b, double c) { return _
 // host-side launchers implemented per dtype (star_f32.cu / star_f64.cu)
 namespace stkb {
 struct StarLaunch {
-    int kind;          // 1 = STAR, 2 = WAVE
+    int kind;          // 1 = STAR, 2 = WAVE, 4 = BOX
     int radius;
     bool has_divisor;
     const CUtensorMap* maps;  // [4]: src halo box, src centre box, prev centre box, vel centre box

@@ -29,7 +29,7 @@
 
 namespace stkb {
 
-enum { FORM_STAR = 0, FORM_STAR_DIV = 1, FORM_WAVE = 2 };
+enum { FORM_STAR = 0, FORM_STAR_DIV = 1, FORM_WAVE = 2, FORM_BOX = 3, FORM_BOX_DIV = 4 };
 
 template <typename T, int R, int FORM, int TY, int NWY>
 struct StarCfg {
@@ -266,149 +266,153 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     mbar_wait(&full[s], ph);
                     const T* t = tiles + size_t(s) * C::STAGE_ELEMS;
 
-                    // centre values of this thread's rows in plane q
-                    T cvs[TY][VEC];
+                    if constexpr (FORM == FORM_BOX || FORM == FORM_BOX_DIV) {
+                        // dense (2R+1)^3 kernel: plane q adds layer dz of the cube to output
+                        // q - dz for every dz; output q + R starts here, q - R completes here
 #pragma unroll
-                    for (int j = 0; j < TY; ++j) lds16(t + (jr0 + j + R) * SW + xl + RA, cvs[j]);
-                    P cv[TY][NPK];
-#pragma unroll
-                    for (int j = 0; j < TY; ++j)
-#pragma unroll
-                        for (int k = 0; k < NPK; ++k) cv[j][k] = K::make(&cvs[j][k * W]);
-
-#ifdef STKB_EXP_NOBRANCH
-                    if (true) {
-#else
-                    if (q >= z0 && q < z1) {
-#endif
-                        // output q: its accumulator already holds the d0 taps of planes < q
-#pragma unroll
-                        for (int j = 0; j < TY; ++j) {
-                            T xr[VEC + 2 * RA];  // left halo | centre | right halo of row j
-                            const T* row = t + (jr0 + j + R) * SW + xl;
+                        for (int rr = 0; rr < TY + 2 * R; ++rr) {
+                            T xr[VEC + 2 * RA];
+                            const T* row = t + (jr0 + rr) * SW + xl;
 #pragma unroll
                             for (int k = 0; k < RA / VEC; ++k) {
                                 lds16(row + k * VEC, &xr[k * VEC]);
                                 lds16(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
                             }
-#pragma unroll
-                            for (int i = 0; i < VEC; ++i) xr[RA + i] = cvs[j][i];
-#pragma unroll
-                            for (int k = 0; k < NPK; ++k) {
-                                P s_ = K::fma(a.c0, cv[j][k], acc[p][j][k]);
-#pragma unroll
-                                for (int m = 1; m <= R; ++m) {
-                                    if (W == 1 || (m % 2) == 0 || !ODD_SCALAR) {
-                                        s_ = K::fma(a.cm[2][m - 1], K::make(&xr[RA + k * W - m]), s_);
-                                        s_ = K::fma(a.cp[2][m - 1], K::make(&xr[RA + k * W + m]), s_);
-                                    } else {  // odd shift: the pair straddles two register pairs
-                                        T l[W], r[W];
-                                        K::put(l, s_);
-#pragma unroll
-                                        for (int w = 0; w < W; ++w) {
-                                            l[w] = fma_t(a.cm[2][m - 1], xr[RA + k * W + w - m], l[w]);
-                                            l[w] = fma_t(a.cp[2][m - 1], xr[RA + k * W + w + m], l[w]);
-                                        }
-                                        (void)r;
-                                        s_ = K::make(l);
-                                    }
-                                }
-                                acc[p][j][k] = s_;
-                            }
-                        }
-#ifdef STKB_EXP_YSPLIT
-                        // d1 (y) taps into a second accumulator chain (shorter FMA dependency chains)
-                        P yacc[TY][NPK];
-#pragma unroll
-                        for (int rr = 0; rr < TY + 2 * R; ++rr) {
-                            T yv[VEC];
-                            if (rr >= R && rr < R + TY) {
-#pragma unroll
-                                for (int i = 0; i < VEC; ++i) yv[i] = cvs[rr - R][i];
-                            } else {
-                                lds16(t + (jr0 + rr) * SW + xl + RA, yv);
-                            }
+                            lds16(row + RA, &xr[RA]);
 #pragma unroll
                             for (int j = 0; j < TY; ++j) {
-                                const int m = rr - (j + R);
-                                if (m != 0 && m >= -R && m <= R) {
-                                    const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
+                                const int dy = rr - (j + R);
+                                if (dy < -R || dy > R) continue;
 #pragma unroll
-                                    for (int k = 0; k < NPK; ++k)
-                                        yacc[j][k] = (m == -R) ? K::mul(c, K::make(&yv[k * W]))
-                                                               : K::fma(c, K::make(&yv[k * W]), yacc[j][k]);
-                                }
-                            }
-                        }
+                                for (int dz = -R; dz <= R; ++dz) {
+                                    constexpr int NS_ = NS;
+                                    const int slot = (p - dz + 2 * NS_) % NS_;
 #pragma unroll
-                        for (int j = 0; j < TY; ++j)
+                                    for (int k = 0; k < NPK; ++k) {
+                                        P s_ = acc[slot][j][k];
 #pragma unroll
-                            for (int k = 0; k < NPK; ++k) acc[p][j][k] = K::fma(T(1), yacc[j][k], acc[p][j][k]);
-#else
-                        // d1 (y) taps: stream the TY+2R rows of this warp's column
+                                        for (int dx = -R; dx <= R; ++dx) {
+                                            const T c = a.cb[((dz + R) * (2 * R + 1) + (dy + R)) * (2 * R + 1) + (dx + R)];
+                                            const int e = RA + k * W + dx;
+                                            const bool first = (dz == -R && dy == -R && dx == -R);
+                                            if (W == 1 || (e % 2) == 0 || !ODD_SCALAR) {
+                                                s_ = first ? K::mul(c, K::make(&xr[e])) : K::fma(c, K::make(&xr[e]), s_);
+                                            } else {
+                                                T l[W];
+                                                K::put(l, s_);
 #pragma unroll
-                        for (int rr = 0; rr < TY + 2 * R; ++rr) {
-                            if (rr >= R && rr < R + TY) {
-#pragma unroll
-                                for (int j = 0; j < TY; ++j) {
-                                    const int m = rr - (j + R);
-                                    if (m != 0 && m >= -R && m <= R) {
-                                        const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
-#pragma unroll
-                                        for (int k = 0; k < NPK; ++k)
-                                            acc[p][j][k] = K::fma(c, cv[rr - R][k], acc[p][j][k]);
-                                    }
-                                }
-                            } else {
-                                T yv[VEC];
-                                lds16(t + (jr0 + rr) * SW + xl + RA, yv);
-#pragma unroll
-                                for (int j = 0; j < TY; ++j) {
-                                    const int m = rr - (j + R);
-                                    if (m >= -R && m <= R) {
-                                        const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
-#pragma unroll
-                                        for (int k = 0; k < NPK; ++k)
-                                            acc[p][j][k] = K::fma(c, K::make(&yv[k * W]), acc[p][j][k]);
+                                                for (int w = 0; w < W; ++w)
+                                                    l[w] = first ? c * xr[e + w] : fma_t(c, xr[e + w], l[w]);
+                                                s_ = K::make(l);
+                                            }
+                                        }
+                                        acc[slot][j][k] = s_;
                                     }
                                 }
                             }
                         }
-#endif
-                    }
-#ifdef STKB_EXP_NOBRANCH
-                    if (true) {
-#else
-                    if (q < z1) {
-#endif
-                        // plane q feeds future outputs q+m with the -m coefficient
-#pragma unroll
+                    } else {
+                        // centre values of this thread's rows in plane q
+                        T cvs[TY][VEC];
+    #pragma unroll
+                        for (int j = 0; j < TY; ++j) lds16(t + (jr0 + j + R) * SW + xl + RA, cvs[j]);
+                        P cv[TY][NPK];
+    #pragma unroll
                         for (int j = 0; j < TY; ++j)
-#pragma unroll
-                            for (int k = 0; k < NPK; ++k) {
-                                acc[(p + R) % NS][j][k] = K::mul(a.cm[0][R - 1], cv[j][k]);
-#pragma unroll
-                                for (int m = 1; m < R; ++m)
-                                    acc[(p + m) % NS][j][k] = K::fma(a.cm[0][m - 1], cv[j][k], acc[(p + m) % NS][j][k]);
-                            }
-                    }
-                    // plane q feeds past outputs q-m with the +m coefficient
-#pragma unroll
-                    for (int j = 0; j < TY; ++j)
-#pragma unroll
-                        for (int k = 0; k < NPK; ++k)
-#pragma unroll
-                            for (int m = 1; m <= R; ++m)
-                                acc[(p - m + NS) % NS][j][k] =
-                                    K::fma(a.cp[0][m - 1], cv[j][k], acc[(p - m + NS) % NS][j][k]);
+    #pragma unroll
+                            for (int k = 0; k < NPK; ++k) cv[j][k] = K::make(&cvs[j][k * W]);
 
+                        if (q >= z0 && q < z1) {
+                            // output q: its accumulator already holds the d0 taps of planes < q
+    #pragma unroll
+                            for (int j = 0; j < TY; ++j) {
+                                T xr[VEC + 2 * RA];  // left halo | centre | right halo of row j
+                                const T* row = t + (jr0 + j + R) * SW + xl;
+    #pragma unroll
+                                for (int k = 0; k < RA / VEC; ++k) {
+                                    lds16(row + k * VEC, &xr[k * VEC]);
+                                    lds16(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
+                                }
+    #pragma unroll
+                                for (int i = 0; i < VEC; ++i) xr[RA + i] = cvs[j][i];
+    #pragma unroll
+                                for (int k = 0; k < NPK; ++k) {
+                                    P s_ = K::fma(a.c0, cv[j][k], acc[p][j][k]);
+    #pragma unroll
+                                    for (int m = 1; m <= R; ++m) {
+                                        if (W == 1 || (m % 2) == 0 || !ODD_SCALAR) {
+                                            s_ = K::fma(a.cm[2][m - 1], K::make(&xr[RA + k * W - m]), s_);
+                                            s_ = K::fma(a.cp[2][m - 1], K::make(&xr[RA + k * W + m]), s_);
+                                        } else {  // odd shift: the pair straddles two register pairs
+                                            T l[W], r[W];
+                                            K::put(l, s_);
+    #pragma unroll
+                                            for (int w = 0; w < W; ++w) {
+                                                l[w] = fma_t(a.cm[2][m - 1], xr[RA + k * W + w - m], l[w]);
+                                                l[w] = fma_t(a.cp[2][m - 1], xr[RA + k * W + w + m], l[w]);
+                                            }
+                                            (void)r;
+                                            s_ = K::make(l);
+                                        }
+                                    }
+                                    acc[p][j][k] = s_;
+                                }
+                            }
+                            // d1 (y) taps: stream the TY+2R rows of this warp's column
+    #pragma unroll
+                            for (int rr = 0; rr < TY + 2 * R; ++rr) {
+                                if (rr >= R && rr < R + TY) {
+    #pragma unroll
+                                    for (int j = 0; j < TY; ++j) {
+                                        const int m = rr - (j + R);
+                                        if (m != 0 && m >= -R && m <= R) {
+                                            const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
+    #pragma unroll
+                                            for (int k = 0; k < NPK; ++k)
+                                                acc[p][j][k] = K::fma(c, cv[rr - R][k], acc[p][j][k]);
+                                        }
+                                    }
+                                } else {
+                                    T yv[VEC];
+                                    lds16(t + (jr0 + rr) * SW + xl + RA, yv);
+    #pragma unroll
+                                    for (int j = 0; j < TY; ++j) {
+                                        const int m = rr - (j + R);
+                                        if (m >= -R && m <= R) {
+                                            const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
+    #pragma unroll
+                                            for (int k = 0; k < NPK; ++k)
+                                                acc[p][j][k] = K::fma(c, K::make(&yv[k * W]), acc[p][j][k]);
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                        if (q < z1) {
+                            // plane q feeds future outputs q+m with the -m coefficient
+    #pragma unroll
+                            for (int j = 0; j < TY; ++j)
+    #pragma unroll
+                                for (int k = 0; k < NPK; ++k) {
+                                    acc[(p + R) % NS][j][k] = K::mul(a.cm[0][R - 1], cv[j][k]);
+    #pragma unroll
+                                    for (int m = 1; m < R; ++m)
+                                        acc[(p + m) % NS][j][k] = K::fma(a.cm[0][m - 1], cv[j][k], acc[(p + m) % NS][j][k]);
+                                }
+                        }
+                        // plane q feeds past outputs q-m with the +m coefficient
+    #pragma unroll
+                        for (int j = 0; j < TY; ++j)
+    #pragma unroll
+                            for (int k = 0; k < NPK; ++k)
+    #pragma unroll
+                                for (int m = 1; m <= R; ++m)
+                                    acc[(p - m + NS) % NS][j][k] =
+                                        K::fma(a.cp[0][m - 1], cv[j][k], acc[(p - m + NS) % NS][j][k]);
+                    }
                     // output plane z = q - R is complete
                     const int z = q - R;
-#ifdef STKB_EXP_NOBRANCH
-                    const bool z_out = (z >= z0);
-#else
                     const bool z_out = (z >= z0) && (z < z1);
-#endif
                     constexpr int ks = (NS - R) % NS;  // slot of output q - R relative to p
                     T outv[TY][VEC];
                     if (z_out) {
@@ -417,7 +421,8 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
 #pragma unroll
                             for (int k = 0; k < NPK; ++k) {
                                 P v = acc[(p + ks) % NS][j][k];
-                                if constexpr (FORM == FORM_STAR_DIV) v = K::mul(a.divisor, v);  // host passes 1/divisor
+                                if constexpr (FORM == FORM_STAR_DIV || FORM == FORM_BOX_DIV)
+                                    v = K::mul(a.divisor, v);  // host passes 1/divisor
                                 if constexpr (FORM == FORM_WAVE) {
                                     const T* cu = t + C::HALO_ELEMS + (jr0 + j) * BX + xl + k * W;
                                     const P uu = K::make(cu);
@@ -571,6 +576,14 @@ inline int star_variant_env() {
 template <typename T, int R, int V>
 cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
     constexpr Variant vv = star_variant_of<T>(R, V);
+    if (L.kind == 4) {
+        if constexpr (R <= 2) {
+            if (L.has_divisor) return launch_star_cfg<T, R, FORM_BOX_DIV, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+            return launch_star_cfg<T, R, FORM_BOX, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    }
     if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
     if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
     return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);

@@ -174,6 +174,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.wave_a = T(d.wave_a);
     a.wave_b = T(d.wave_b);
     a.store_hint = dom->store_hint;
+    if (d.kind == STKB_MAP_BOX)
+        for (int i = 0; i < 125; ++i) a.cb[i] = T(d.box_coef[i]);
 
     int bx, by, hx;
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
@@ -463,9 +465,10 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     MapOp op;
     op.d = d;
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
-    if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE) {
+    if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX) {
         if (nd != 3) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels need a 3-D grid");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
+        if (d.kind == STKB_MAP_BOX && d.radius > 2) return fail(STKB_ERR_UNSUPPORTED, "streaming box kernels cover radius 1..2");
         if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");
         if (int rc = check_name(dom, d.src, "src")) return rc;
         if (int rc = check_name(dom, d.dst, "dst")) return rc;

@@ -8,8 +8,9 @@ here the update expression is expanded into a polynomial over grid reads
 
   STAR  v[0] = (sum_k c_k * u[o_k]) [/ d]      star offsets, radius 1..4, 3-D
   WAVE  w[0] = a*u[0] + b*p[0] + k[0] * (sum_k c_k * u[o_k])
+  BOX   v[0] = (sum over the dense (2R+1)^3 cube) [/ d]   box / "other", R <= 2
 
-Everything else — box/"other" shapes, locals, several updates, 2-D maps,
+Everything else — larger box/"other" shapes, several updates, 2-D maps,
 in-place Jacobi updates, offset destinations, or ``precision="exact"`` —
 compiles to EXPR bytecode, which the device evaluates in float64 in parse
 order with one rounding per store (bit-identical to run_target).
@@ -23,6 +24,7 @@ from typing import Optional
 from .program import node_kind
 
 MAX_FAST_RADIUS = 4
+MAX_BOX_RADIUS = 2
 
 
 class MatchError(ValueError):
@@ -31,13 +33,13 @@ class MatchError(ValueError):
 
 @dataclass
 class MapPlan:
-    kind: str  # "star" | "wave" | "expr"
+    kind: str  # "star" | "wave" | "box" | "expr"
     radius: int = 0
     src: Optional[str] = None  # module grid names
     dst: Optional[str] = None
     prev: Optional[str] = None
     vel: Optional[str] = None
-    coef: list = field(default_factory=list)  # 6R+1, C-ABI layout
+    coef: list = field(default_factory=list)  # star: 6R+1, C-ABI layout; box: (2R+1)^3 dense cube
     divisor: float = 0.0
     wave_a: float = 0.0
     wave_b: float = 0.0
@@ -189,9 +191,19 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
             raise MatchError("weighted sum over several grids")
         src_param = grids.pop()
         offs = [k[0][1] for k in deg1]
-        if not _is_star(offs, 3):
-            raise MatchError("not star-shaped")
         r = max(max(abs(c) for c in o) for o in offs)
+        if not _is_star(offs, 3):
+            if r > MAX_BOX_RADIUS:
+                raise MatchError(f"box/other shape of radius {r} (dense streaming kernel covers <= {MAX_BOX_RADIUS})")
+            src = params[src_param]
+            if src == dst:
+                raise MatchError("in-place update (reads and writes the same grid)")
+            n = 2 * r + 1
+            cube = [0.0] * n ** 3
+            for k, v in deg1.items():
+                dz, dy, dx = k[0][1]
+                cube[((dz + r) * n + (dy + r)) * n + (dx + r)] = v
+            return MapPlan("box", r, src, dst, coef=cube, divisor=divisor, box=box)
         if r < 1 or r > MAX_FAST_RADIUS:
             raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
         src = params[src_param]

@@ -60,8 +60,8 @@ def test_library_rejects_bad_descriptors_without_gpu():
 
 @pytest.mark.parametrize("builder,kind", [("star3d4r", "star"), ("star3d1r", "star"), ("star3d2r", "star"),
                                           ("star3d3r", "star"), ("star3d4r_norm", "star"), ("jacobi7", "star"),
-                                          ("wave", "wave"), ("j3d27pt", "expr"), ("box3d2r", "expr"),
-                                          ("star2d4r", "expr")])
+                                          ("wave", "wave"), ("j3d27pt", "box"), ("box3d2r", "box"),
+                                          ("box3d1r", "box"), ("box3d3r", "expr"), ("star2d4r", "expr")])
 def test_matcher_routes(builder, kind):
     shape = (16, 16) if builder.startswith("star2d") else (16, 16, 16)
     bound, _ = corpus.config_target(builder, shape, 1)

@@ -63,13 +63,13 @@ def test_fast_within_tolerance_vs_reference_golden(case, template):
 
 
 def test_fast_path_is_taken_for_star_and_wave():
-    for builder in ("star3d4r", "star3d1r", "wave", "star3d4r_norm", "jacobi7"):
+    for builder in ("star3d4r", "star3d1r", "wave", "star3d4r_norm", "jacobi7", "j3d27pt", "box3d2r"):
         bound, decls = corpus.config_target(builder, (16, 16, 16), 1)
         grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
         with DeviceTarget(grids) as dt:
             bmap = next(_maps(bound.stmts))
             dt.compile_map(bmap, 0)
-            assert dt.plans[0].kind in ("star", "wave"), (builder, dt.plans[0].reason)
+            assert dt.plans[0].kind in ("star", "wave", "box"), (builder, dt.plans[0].reason)
 
 
 @pytest.mark.parametrize("shape", [(37, 45, 133), (9, 70, 250), (128, 128, 128)])
@@ -81,6 +81,19 @@ def test_fast_ragged_and_c1_shapes_vs_c_oracle(shape, kernel):
     fill_loguniform(grids["u"], 7)
     ref = oracle.run_target_c(bound, grids)
     got = run_gpu(bound, _plan(bound), grids)
+    for n in ref:
+        rep = compare(ref[n], got[n])
+        assert rep.max_relative <= 1e-5, (kernel, shape, n, rep.render())
+
+
+@pytest.mark.parametrize("shape", [(37, 45, 133), (64, 64, 64)])
+@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r"])
+def test_fast_box_kernels_vs_c_oracle(shape, kernel):
+    bound, decls = corpus.config_target(kernel, shape, 3)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 4)
+    ref = oracle.run_target_c(bound, grids)
+    got = run_gpu(bound, _plan(bound, "smem"), grids)
     for n in ref:
         rep = compare(ref[n], got[n])
         assert rep.max_relative <= 1e-5, (kernel, shape, n, rep.render())

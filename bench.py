@@ -136,9 +136,12 @@ def fill_device(dt, names, shape, builder, seed=7):
     for n in names:
         flat = device_view(dt.device_ptr(n), lay["elems"], tdt)
         flat.zero_()
-    interior = {n: device_view(dt.device_ptr(n), lay["elems"], tdt).as_strided(
-        shape, (lay["plane"], lay["pitch"], 1), o * lay["plane"] + o * lay["pitch"] + lay["lead"]) for n in names}
-    for z in range(0, shape[0], 64):  # bounded temporaries
+    if len(shape) == 3:
+        strides, off = (lay["plane"], lay["pitch"], 1), o * lay["plane"] + o * lay["pitch"] + lay["lead"]
+    else:  # 2-D grids are lifted to one plane of n0 rows
+        strides, off = (lay["pitch"], 1), o * lay["pitch"] + lay["lead"]
+    interior = {n: device_view(dt.device_ptr(n), lay["elems"], tdt).as_strided(shape, strides, off) for n in names}
+    for z in range(0, shape[0], 64 if len(shape) == 3 else shape[0]):  # bounded temporaries
         sl = interior[names[0]][z:z + 64]
         synthetic_log_uniform(sl, seed + z)
     if builder == "wave":

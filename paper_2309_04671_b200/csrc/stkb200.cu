@@ -27,6 +27,19 @@ cudaError_t launch_expr(int dtype, const Geometry& g, const Box& box, const int3
 cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const void* got, void* partials,
                            int blocks, cudaStream_t s);
 size_t compare_partial_bytes();
+struct Star2DArgs {
+    int64_t pitch;
+    int64_t lead;
+    int32_t order;
+    int32_t lo0, hi0, lo1, hi1;
+    int32_t x0base;
+    int32_t n_tx, lz, n_tz;
+    int32_t* nonfinite;
+    double c0, cm0[4], cp0[4], cm1[4], cp1[4];
+    double rdiv;
+};
+cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
+                          cudaStream_t s);
 }  // namespace stkb
 
 using namespace stkb;
@@ -148,9 +161,35 @@ Box box_of(const stkb_map_desc& d) {
     return b;
 }
 
+// 2-D star maps: the 1.5-D streaming kernel (d0 streamed, d1 on lanes)
+int launch_star2d_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind) {
+    const stkb_map_desc& d = op.d;
+    Star2DArgs a{};
+    a.pitch = dom->g.pitch;
+    a.lead = dom->g.lead;
+    a.order = int32_t(dom->g.order);
+    a.lo0 = int32_t(d.lo[1]); a.hi0 = int32_t(d.hi[1]);  // lifted: d0 of the 2-D grid is the row axis
+    a.lo1 = int32_t(d.lo[2]); a.hi1 = int32_t(d.hi[2]);
+    a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
+    const int R = d.radius;
+    a.c0 = d.coef[0];
+    for (int m = 1; m <= 4; ++m) {
+        a.cm0[m - 1] = m <= R ? d.coef[1 + 2 * (m - 1)] : 0.0;
+        a.cp0[m - 1] = m <= R ? d.coef[1 + 2 * (m - 1) + 1] : 0.0;
+        a.cm1[m - 1] = m <= R ? d.coef[1 + 2 * R + 2 * (m - 1)] : 0.0;
+        a.cp1[m - 1] = m <= R ? d.coef[1 + 2 * R + 2 * (m - 1) + 1] : 0.0;
+    }
+    a.rdiv = d.divisor != 0.0 ? 1.0 / d.divisor : 0.0;
+    cudaError_t e = launch_star2d(dom->desc.dtype, a, R, dom->bufs[bind[d.src]], dom->bufs[bind[d.dst]],
+                                  d.divisor != 0.0, dom->num_sms, dom->stream);
+    if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("2-D star kernel launch: ") + cudaGetErrorString(e));
+    return STKB_OK;
+}
+
 template <typename T>
 int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind) {
     const stkb_map_desc& d = op.d;
+    if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
     StarArgs<T> a{};
     a.g = dom->g;
     a.box = box_of(d);
@@ -466,7 +505,8 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     op.d = d;
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
     if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX) {
-        if (nd != 3) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels need a 3-D grid");
+        if (nd != 3 && !(nd == 2 && d.kind == STKB_MAP_STAR))
+            return fail(STKB_ERR_UNSUPPORTED, "2-D grids stream star maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
         if (d.kind == STKB_MAP_BOX && d.radius > 2) return fail(STKB_ERR_UNSUPPORTED, "streaming box kernels cover radius 1..2");
         if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");

@@ -163,8 +163,8 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
         raise MatchError("several updates in one kernel")
     upd = kern.updates[0]
     dims = len(upd.offset)
-    if dims != 3:
-        raise MatchError(f"{dims}-D kernel (the streaming kernels are 3-D)")
+    if dims not in (2, 3):
+        raise MatchError(f"{dims}-D kernel (the streaming kernels are 2-D and 3-D)")
     if any(upd.offset):
         raise MatchError("destination offset is not the centre")
     scalars = {n: float(v) for n, v in bmap.scalar_args}
@@ -192,7 +192,9 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
         src_param = grids.pop()
         offs = [k[0][1] for k in deg1]
         r = max(max(abs(c) for c in o) for o in offs)
-        if not _is_star(offs, 3):
+        if dims == 2 and not _is_star(offs, 2):
+            raise MatchError("2-D box/other shape")
+        if dims == 3 and not _is_star(offs, 3):
             if r > MAX_BOX_RADIUS:
                 raise MatchError(f"box/other shape of radius {r} (dense streaming kernel covers <= {MAX_BOX_RADIUS})")
             src = params[src_param]
@@ -216,6 +218,8 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
 
     if divisor:
         raise MatchError("divided wave form")
+    if dims != 3:
+        raise MatchError("2-D degree-2 form")
     # WAVE: deg-2 terms are vel[0] * u[o]
     vel_cands = None
     for k in deg2:

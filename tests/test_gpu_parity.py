@@ -86,6 +86,19 @@ def test_fast_ragged_and_c1_shapes_vs_c_oracle(shape, kernel):
         assert rep.max_relative <= 1e-5, (kernel, shape, n, rep.render())
 
 
+@pytest.mark.parametrize("shape", [(1000, 1000), (37, 133), (9, 700)])
+@pytest.mark.parametrize("kernel", ["star2d4r", "star2d1r", "j2d5pt", "j2d9pt", "star2d3r"])
+def test_fast_2d_streaming_vs_c_oracle(shape, kernel):
+    bound, decls = corpus.config_target(kernel, shape, 5)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 6)
+    ref = oracle.run_target_c(bound, grids)
+    got = run_gpu(bound, _plan(bound, "shift"), grids)
+    for n in ref:
+        rep = compare(ref[n], got[n])
+        assert rep.max_relative <= 1e-5, (kernel, shape, n, rep.render())
+
+
 @pytest.mark.parametrize("shape", [(37, 45, 133), (64, 64, 64)])
 @pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r"])
 def test_fast_box_kernels_vs_c_oracle(shape, kernel):

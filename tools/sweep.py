@@ -34,7 +34,7 @@ def time_one(builder, shape, dtype, steps=20, warm=3):
     ms = dt.elapsed_ms() / steps
     kind = dt.plans[0].kind
     dt.close()
-    bpp = (16 if builder == "wave" else 8) * (2 if dtype == "f64" else 1)
+    bpp = (16 if builder == "wave" else 8) * (2 if dtype == "f64" else 1)  # algorithmic bytes per point
     pts = int(np.prod(shape))
     return dict(builder=builder, shape=shape, dtype=dtype, kind=kind, ms=round(ms, 4),
                 gpts=round(pts / ms / 1e6, 1), gbs=round(pts * bpp / ms / 1e6, 1))

@@ -24,9 +24,16 @@ struct Star2DArgs {
     double rdiv;     // 1/divisor or 0
 };
 
+// the same coefficients in the grid dtype, read straight from the parameter bank
+template <typename T>
+struct Coef2D {
+    T c0, cm0[4], cp0[4], cm1[4], cp1[4], rdiv;
+};
+
 template <typename T, int R, bool DIV>
 __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                     const __grid_constant__ Star2DArgs a) {
+                                                     const __grid_constant__ Star2DArgs a,
+                                                     const __grid_constant__ Coef2D<T> cf) {
     using K = Pk<T>;
     using P = typename K::P;
     constexpr int VEC = 16 / sizeof(T);
@@ -44,13 +51,12 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
     const int nq = (z1 - z0) + 2 * R;
     const bool x_full = x >= a.lo1 && x + VEC <= a.hi1;
     const bool x_any = x + VEC > a.lo1 && x < a.hi1;
-    const T c0 = T(a.c0);
-    T cmz[4], cpz[4], cmx[4], cpx[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        cmz[m] = T(a.cm0[m]); cpz[m] = T(a.cp0[m]); cmx[m] = T(a.cm1[m]); cpx[m] = T(a.cp1[m]);
-    }
-    const T rdiv = T(a.rdiv);
+    const T c0 = cf.c0;
+    const T* cmz = cf.cm0;
+    const T* cpz = cf.cp0;
+    const T* cmx = cf.cm1;
+    const T* cpx = cf.cp1;
+    const T rdiv = cf.rdiv;
     const T* row0 = src + a.lead + x;  // + (q + order) * pitch
     T* out0 = dst + a.lead + x;
     P acc[NS][NPK];
@@ -59,6 +65,11 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
 #pragma unroll
         for (int i = 0; i < NPK; ++i) acc[k][i] = K::mul(T(0), P{});
     P chk = K::mul(T(0), P{});
+    T nx[VEC + 2 * RA];  // prefetched next row: left halo | centre | right halo
+    {
+        const T* nrow = row0 + int64_t(z0 - R + a.order) * a.pitch;  // first row (a warm-up row: centre only)
+        ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&nx[RA]));
+    }
 
     for (int qb = 0; qb < nq; qb += NS) {
 #pragma unroll
@@ -66,18 +77,25 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
             const int qi = qb + p;
             if (qi >= nq) break;
             const int q = z0 - R + qi;
-            const T* row = row0 + int64_t(q + a.order) * a.pitch;
+            // this row was fetched one step ahead (nx); fetch the next one now
             T xr[VEC + 2 * RA];
-            ldg16(row, *reinterpret_cast<T(*)[VEC]>(&xr[RA]));
+#pragma unroll
+            for (int i = 0; i < VEC + 2 * RA; ++i) xr[i] = nx[i];
+            if (qi + 1 < nq) {
+                const T* nrow = row0 + int64_t(q + 1 + a.order) * a.pitch;
+                ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&nx[RA]));
+                if (q + 1 >= z0 && q + 1 < z1) {
+#pragma unroll
+                    for (int k = 0; k < RA / VEC; ++k) {
+                        ldg16(nrow - RA + k * VEC, *reinterpret_cast<T(*)[VEC]>(&nx[k * VEC]));
+                        ldg16(nrow + VEC + k * VEC, *reinterpret_cast<T(*)[VEC]>(&nx[RA + VEC + k * VEC]));
+                    }
+                }
+            }
             P cv[NPK];
 #pragma unroll
             for (int k = 0; k < NPK; ++k) cv[k] = K::make(&xr[RA + k * W]);
             if (q >= z0 && q < z1) {
-#pragma unroll
-                for (int k = 0; k < RA / VEC; ++k) {
-                    ldg16(row - RA + k * VEC, *reinterpret_cast<T(*)[VEC]>(&xr[k * VEC]));
-                    ldg16(row + VEC + k * VEC, *reinterpret_cast<T(*)[VEC]>(&xr[RA + VEC + k * VEC]));
-                }
 #pragma unroll
                 for (int k = 0; k < NPK; ++k) {
                     P s_ = K::fma(c0, cv[k], acc[p][k]);
@@ -141,10 +159,16 @@ template <typename T, int R>
 cudaError_t launch2d_r(const Star2DArgs& a, const void* src, void* dst, bool div, cudaStream_t s) {
     const int warps = a.n_tx * a.n_tz;
     const int blocks = (warps + 3) / 4;
+    Coef2D<T> cf;
+    cf.c0 = T(a.c0);
+    for (int m = 0; m < 4; ++m) {
+        cf.cm0[m] = T(a.cm0[m]); cf.cp0[m] = T(a.cp0[m]); cf.cm1[m] = T(a.cm1[m]); cf.cp1[m] = T(a.cp1[m]);
+    }
+    cf.rdiv = T(a.rdiv);
     if (div)
-        star2d_kernel<T, R, true><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a);
+        star2d_kernel<T, R, true><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
     else
-        star2d_kernel<T, R, false><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a);
+        star2d_kernel<T, R, false><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
     return cudaGetLastError();
 }
 

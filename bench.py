@@ -192,16 +192,21 @@ def run_ours(args) -> None:
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     builder, shape, dtype, bpp, ref_name = CONFIGS[args.config]
     K, W = args.steps, args.warmup
     peaks = measured_peaks()
     npts = int(np.prod(shape))
 
-    if ws == 1:
+    if ws == 1 and not args.force_slabs:
         bound, decls = corpus.config_target(builder, shape, K, dtype)
         names = list(decls)
         body = next(s for s in bound.stmts if type(s).__name__ == "BoundFor").body
@@ -233,7 +238,7 @@ def run_ours(args) -> None:
         local_pts = sb.local_points
         comm = sb.comm_info()
         sb.close()
-    if ws > 1:
+    if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -246,7 +251,7 @@ def run_ours(args) -> None:
 
     # ------------------------------------------------------------ end to end
     e2e = None
-    if not args.no_e2e and ws == 1:
+    if not args.no_e2e and ws == 1 and not args.force_slabs:
         bound, decls = corpus.config_target(builder, shape, K, dtype)
         grids = pinned_grids(decls, builder)
         bmap = next(s for s in next(s for s in bound.stmts if type(s).__name__ == "BoundFor").body
@@ -316,7 +321,7 @@ def run_ours(args) -> None:
         if comm:
             line["config"]["halo_exchange"] = comm
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
         dist.barrier()
@@ -365,6 +370,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="use the z-slab/NCCL engine even on one GPU (tests the multi-GPU path)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="DRAM bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()

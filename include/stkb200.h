@@ -152,6 +152,17 @@ int stkb_nonfinite(stkb_domain *dom, int32_t tag, int32_t *flag); /* sticky; cle
  * planes (interior index z0, may be negative for halo planes) of the buffer a
  * name is bound to, for halo exchange over NCCL / peer memory. */
 int stkb_launch_map(stkb_domain *dom, int32_t map_index, int64_t lo0, int64_t hi0);
+/* One launch over several disjoint d0 ranges; the first n_signal ranges are
+ * scheduled first and every stored item of them adds 1 to the map's signal
+ * counter (*signal_items = how much this launch adds once they are all stored).
+ * The counter only grows (it is never reset, so a waiter can never see a stale
+ * value): the caller keeps the running sum and stkb_stream_wait_signal makes
+ * `stream` (e.g. the halo-exchange stream) wait, without occupying an SM,
+ * until the counter reaches it (cyclic >= comparison). */
+int stkb_launch_map_ranges(stkb_domain *dom, int32_t map_index, int32_t n_ranges, const int64_t *lo0,
+                           const int64_t *hi0, int32_t n_signal, int32_t *signal_items);
+int stkb_stream_wait_signal(stkb_domain *dom, void *stream, int32_t map_index, int32_t value);
+int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (leave SMs for NCCL) */
 int stkb_apply_swap(stkb_domain *dom, int32_t a, int32_t b);
 int stkb_plane_span(stkb_domain *dom, int32_t name, int64_t z0, int64_t nplanes, void **dptr,
                     int64_t *bytes);

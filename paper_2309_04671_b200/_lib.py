@@ -32,7 +32,8 @@ EXPORTS = (
     "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_program_reset",
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
-    "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span",
+    "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
+    "stkb_stream_wait_signal", "stkb_set_max_ctas",
 )
 
 
@@ -124,6 +125,9 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_launch_map": [V, i32, i64, i64],
         "stkb_apply_swap": [V, i32, i32],
         "stkb_plane_span": [V, i32, i64, i64, P(V), P(i64)],
+        "stkb_launch_map_ranges": [V, i32, i32, P(i64), P(i64), i32, P(i32)],
+        "stkb_stream_wait_signal": [V, V, i32, i32],
+        "stkb_set_max_ctas": [V, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -37,8 +37,10 @@ struct StarArgs {
     Box box;
     int32_t x0base;            // lo2 rounded down to the vector width
     int32_t n_tx, n_ty, n_tz;  // work-item grid: x tiles, y tiles, z chunks
-    int32_t lz;                // nominal z-chunk length (chunk bounds in zc)
-    int32_t zc[kMaxChunks + 1];  // z-chunk boundaries relative to box.lo0 (tapered at the end)
+    int32_t lz;                // nominal z-chunk length
+    int32_t zs[2 * kMaxChunks];  // z-chunk t = [zs[2t], zs[2t+1]) (interior d0 coordinates)
+    int32_t n_signal;          // items of chunks t < n_signal bump *signal when stored
+    int32_t* signal;
     int32_t n_items;
     T* dst;
     const T* src;              // centre re-read (WAVE)
@@ -53,6 +55,7 @@ struct StarArgs {
     T wave_a, wave_b;
     T cb[125];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 2
     int32_t store_hint;        // 1: streaming (evict-first) output stores
+    int32_t order_y_fast;      // work items walk y tiles fastest
 };
 
 // ---------------------------------------------------------------------------
@@ -171,6 +174,12 @@ struct StarLaunch {
     int max_ctas;      // 0 = auto (one per SM)
     int lz;            // 0 = auto
     bool taper;        // shorten the last z-chunks
+    int n_ranges;      // 0: one range = the map box; else disjoint d0 ranges, launched as one grid
+    const int32_t* rlo;
+    const int32_t* rhi;
+    int n_signal_ranges;   // the first ranges are "signal" ranges (one chunk each)
+    int32_t* signal;       // counter bumped once per stored signal item
+    int* signal_items;     // out: number of signal items of this launch
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);

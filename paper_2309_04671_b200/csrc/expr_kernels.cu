@@ -170,4 +170,16 @@ cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const 
 
 size_t compare_partial_bytes() { return sizeof(ComparePartial); }
 
+__global__ void signal_add_kernel(int32_t* p, int32_t v) {
+    __threadfence();
+    atomicAdd(p, v);
+}
+
+// stream-ordered "these launches are done" marker for maps without an in-kernel
+// signal; like the in-kernel one it only ever adds (the waiter tracks the sum)
+cudaError_t launch_signal_add(int32_t* p, int32_t v, cudaStream_t s) {
+    signal_add_kernel<<<1, 1, 0, s>>>(p, v);
+    return cudaGetLastError();
+}
+
 }  // namespace stkb

@@ -23,6 +23,7 @@
 //    stage as extra TMA centre boxes, so the epilogue never waits on HBM.
 #pragma once
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -112,6 +113,22 @@ template <> struct Pk<double> {
     static __device__ __forceinline__ bool clean(P chk) { return chk.x == 0.0; }
 };
 
+// work item -> (x tile, y tile, z chunk); z-major so concurrent items are
+// neighbours.  order_y_fast walks y tiles fastest (experiment switch).
+template <typename A>
+__device__ __forceinline__ void decode_item(const A& a, int item, int& tx, int& ty, int& tz) {
+    const int per = a.n_tx * a.n_ty;
+    tz = item / per;
+    const int r = item - tz * per;
+    if (a.order_y_fast) {
+        ty = r % a.n_ty;
+        tx = r / a.n_ty;
+    } else {
+        tx = r % a.n_tx;
+        ty = r / a.n_tx;
+    }
+}
+
 // cold path: one output row of a tile that straddles the region box
 template <typename T>
 __device__ __noinline__ void store_row_masked(T* dz, T v0, T v1, T v2, T v3, int x, int lo2, int hi2) {
@@ -177,14 +194,12 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     mbar_arrive(&full[s]);
                     break;
                 }
-                const int tx = item % a.n_tx;
-                const int rest = item / a.n_tx;
-                const int ty = rest % a.n_ty;
-                const int tz = rest / a.n_ty;
+                int tx, ty, tz;
+                decode_item(a, item, tx, ty, tz);
                 const int x0 = a.x0base + tx * BX;
                 const int y0 = a.box.lo1 + ty * BY;
-                const int z0 = a.box.lo0 + a.zc[tz];
-                const int z1 = a.box.lo0 + a.zc[tz + 1];
+                const int z0 = a.zs[2 * tz];
+                const int z1 = a.zs[2 * tz + 1];
                 const int c0 = int(a.g.lead) + x0 - RA;
                 const int c1 = y0 + int(a.g.order) - R;
                 for (int q = z0 - R; q < z1 + R; ++q, ++it) {
@@ -239,14 +254,12 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
         const int item = stage_item[it % STAGES];
         if (item < 0) break;
-        const int tx = item % a.n_tx;
-        const int rest = item / a.n_tx;
-        const int ty = rest % a.n_ty;
-        const int tz = rest / a.n_ty;
+        int tx, ty, tz;
+        decode_item(a, item, tx, ty, tz);
         const int x0 = a.x0base + tx * BX;
         const int y0 = a.box.lo1 + ty * BY;
-        const int z0 = a.box.lo0 + a.zc[tz];
-        const int z1 = a.box.lo0 + a.zc[tz + 1];
+        const int z0 = a.zs[2 * tz];
+        const int z1 = a.zs[2 * tz + 1];
         const int x = x0 + xl;
         const int nq = (z1 - z0) + 2 * R;
         const bool full_tile = x0 >= a.box.lo2 && x0 + BX <= a.box.hi2 && y0 >= a.box.lo1 && y0 + BY <= a.box.hi1;
@@ -462,6 +475,12 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 }
             }
         }
+        if (tz < a.n_signal) {
+            // a boundary item is stored: publish it (halo exchange waits on the counter)
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"r"(NWY * 32) : "memory");
+            if (threadIdx.x == 0) atomicAdd(a.signal, 1);
+        }
     }
     if (__any_sync(0xffffffffu, !K::clean(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
@@ -486,9 +505,10 @@ inline int choose_lz(int n0, int tiles, int ctas, int R, int* n_tz) {
     return best;
 }
 
-// z-chunk boundaries: uniform chunks of `lz`, except that the last chunks halve
-// (lz/2, lz/4, ... >= 16) so the scheduler's final round is short (smaller tail)
-inline void chunk_bounds(int n0, int lz, int tiles, int ctas, bool taper, int32_t* zc, int32_t* n_tz) {
+// z-chunks of one d0 range [lo, lo+n0): uniform chunks of `lz`, except that the
+// last chunks halve (lz/2, lz/4, ... >= 16) so the scheduler's final round is
+// short (smaller tail).  Appends (lo, hi) pairs to zs; returns the new count.
+inline int chunk_range(int lo, int n0, int lz, int tiles, int ctas, bool taper, int32_t* zs, int k) {
     int tail[16], nt = 0, tail_sum = 0;
     if (taper && 2 * tiles >= ctas)
         for (int l = lz / 2; l >= 16 && nt < 16; l /= 2) {
@@ -500,17 +520,23 @@ inline void chunk_bounds(int n0, int lz, int tiles, int ctas, bool taper, int32_
         nt = 0;
         main_len = n0;
     }
-    int k = 0;
-    zc[k++] = 0;
     const int n_main = (main_len + lz - 1) / lz;
-    for (int c = 1; c <= n_main && k <= kMaxChunks; ++c) zc[k++] = int32_t((int64_t(main_len) * c) / n_main);
-    int z = main_len;
-    for (int i = 0; i < nt && k <= kMaxChunks; ++i) {
-        z += tail[i];
-        zc[k++] = z;
+    int prev = 0;
+    for (int c = 1; c <= n_main && k < kMaxChunks; ++c) {
+        const int z = int((int64_t(main_len) * c) / n_main);
+        zs[2 * k] = lo + prev;
+        zs[2 * k + 1] = lo + z;
+        prev = z;
+        ++k;
     }
-    zc[k - 1] = n0;
-    *n_tz = k - 1;
+    for (int i = 0; i < nt && k < kMaxChunks; ++i) {
+        zs[2 * k] = lo + prev;
+        zs[2 * k + 1] = lo + prev + tail[i];
+        prev += tail[i];
+        ++k;
+    }
+    zs[2 * k - 1] = lo + n0;  // close exactly (also if kMaxChunks truncated the list)
+    return k;
 }
 
 template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
@@ -529,18 +555,44 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     const int n0 = a.box.hi0 - a.box.lo0;
     const int tiles = a.n_tx * a.n_ty;
     int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
+    // d0 ranges: the map box, or the caller's list (signal ranges first, one chunk each)
+    int32_t rlo[kMaxChunks], rhi[kMaxChunks];
+    int nr = 0;
+    if (L.n_ranges <= 0) {
+        rlo[0] = a.box.lo0;
+        rhi[0] = a.box.hi0;
+        nr = 1;
+    } else {
+        for (int i = 0; i < L.n_ranges && nr < kMaxChunks; ++i)
+            if (L.rhi[i] > L.rlo[i]) {
+                rlo[nr] = L.rlo[i];
+                rhi[nr] = L.rhi[i];
+                ++nr;
+            }
+    }
+    const int nsig = L.n_ranges > 0 ? std::min(L.n_signal_ranges, nr) : 0;
+    int main_n0 = 0;
+    for (int i = nsig; i < nr; ++i) main_n0 = std::max(main_n0, rhi[i] - rlo[i]);
     if (L.lz > 0) {
         a.lz = L.lz;
-        a.n_tz = (n0 + L.lz - 1) / L.lz;
+    } else if (main_n0 > 0) {
+        int ntz;
+        a.lz = choose_lz(main_n0, tiles, ctas, R, &ntz);
+        if (ntz > kMaxChunks / 2) a.lz = (main_n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
     } else {
-        a.lz = choose_lz(n0, tiles, ctas, R, &a.n_tz);
+        a.lz = 1;
     }
-    if (a.n_tz > kMaxChunks) {
-        a.n_tz = kMaxChunks;
-        a.lz = (n0 + kMaxChunks - 1) / kMaxChunks;
-        a.n_tz = (n0 + a.lz - 1) / a.lz;
+    int k = 0;
+    for (int i = 0; i < nsig && k < kMaxChunks; ++i, ++k) {
+        a.zs[2 * k] = rlo[i];
+        a.zs[2 * k + 1] = rhi[i];
     }
-    chunk_bounds(n0, a.lz, tiles, ctas, L.taper, a.zc, &a.n_tz);
+    for (int i = nsig; i < nr && k < kMaxChunks; ++i)
+        k = chunk_range(rlo[i], rhi[i] - rlo[i], a.lz, tiles, ctas, L.taper, a.zs, k);
+    a.n_tz = k;
+    a.n_signal = nsig;
+    a.signal = L.signal;
+    if (L.signal_items) *L.signal_items = tiles * nsig;
     a.n_items = tiles * a.n_tz;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;

@@ -27,6 +27,7 @@ cudaError_t launch_expr(int dtype, const Geometry& g, const Box& box, const int3
 cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const void* got, void* partials,
                            int blocks, cudaStream_t s);
 size_t compare_partial_bytes();
+cudaError_t launch_signal_add(int32_t* p, int32_t v, cudaStream_t s);
 struct Star2DArgs {
     int64_t pitch;
     int64_t lead;
@@ -122,6 +123,7 @@ struct stkb_domain {
     int l2promo = 3;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
     bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
+    int order_y_fast = 0; // STKB_ORDER_Y=1: work items walk y tiles fastest
 };
 
 namespace {
@@ -186,8 +188,17 @@ int launch_star2d_map(stkb_domain* dom, const MapOp& op, const std::vector<int32
     return STKB_OK;
 }
 
+struct RangeSpec {
+    int n = 0;
+    const int32_t* lo = nullptr;
+    const int32_t* hi = nullptr;
+    int n_signal = 0;
+    int* signal_items = nullptr;
+};
+
 template <typename T>
-int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind) {
+int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind,
+                    const RangeSpec& rs = RangeSpec()) {
     const stkb_map_desc& d = op.d;
     if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
     StarArgs<T> a{};
@@ -213,6 +224,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.wave_a = T(d.wave_a);
     a.wave_b = T(d.wave_b);
     a.store_hint = dom->store_hint;
+    a.order_y_fast = dom->order_y_fast;
     if (d.kind == STKB_MAP_BOX)
         for (int i = 0; i < 125; ++i) a.cb[i] = T(d.box_coef[i]);
 
@@ -242,6 +254,12 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;
     L.taper = dom->taper;
+    L.n_ranges = rs.n;
+    L.rlo = rs.lo;
+    L.rhi = rs.hi;
+    L.n_signal_ranges = rs.n_signal;
+    L.signal = dom->d_flags + kMaxTags + kMaxMaps + op.slot;
+    L.signal_items = rs.signal_items;
     cudaError_t e;
     if constexpr (sizeof(T) == 4) e = launch_star_f32(L, a, dom->stream);
     else e = launch_star_f64(L, a, dom->stream);
@@ -374,14 +392,16 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (cudaStreamCreateWithFlags(&dom->own_stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup("stream");
     dom->stream = dom->own_stream;
     if (cudaEventCreate(&dom->ev0) != cudaSuccess || cudaEventCreate(&dom->ev1) != cudaSuccess) return cleanup("event");
-    // [0, kMaxTags): sticky non-finite flags per map tag; then one scheduler counter per map
-    if (cudaMalloc(&dom->d_flags, (kMaxTags + kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
-    cudaMemset(dom->d_flags, 0, (kMaxTags + kMaxMaps) * sizeof(int32_t));
+    // [0, kMaxTags): sticky non-finite flags per map tag; then one scheduler counter
+    // per map; then one boundary-signal counter per map (slab halo exchange)
+    if (cudaMalloc(&dom->d_flags, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
+    cudaMemset(dom->d_flags, 0, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t));
     if (const char* s = getenv("STKB_LZ")) dom->lz_override = atoi(s);
     if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
     if (const char* s = getenv("STKB_L2PROMO")) dom->l2promo = atoi(s);
     if (const char* s = getenv("STKB_STORE_HINT")) dom->store_hint = atoi(s);
     if (const char* s = getenv("STKB_TAPER")) dom->taper = atoi(s) != 0;
+    if (const char* s = getenv("STKB_ORDER_Y")) dom->order_y_fast = atoi(s);
     *out = dom;
     return STKB_OK;
 }
@@ -728,6 +748,80 @@ int stkb_launch_map(stkb_domain* dom, int32_t map_index, int64_t lo0, int64_t hi
     }
     op.d = saved;
     return rc;
+}
+
+int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges, const int64_t* lo0,
+                           const int64_t* hi0, int32_t n_signal, int32_t* signal_items) {
+    if (!dom || (n_ranges > 0 && (!lo0 || !hi0))) return fail(STKB_ERR_ARG, "null argument");
+    if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
+    if (n_ranges < 0 || n_ranges > 64 || n_signal < 0 || n_signal > n_ranges)
+        return fail(STKB_ERR_ARG, "bad range list");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    MapOp& op = dom->maps[map_index];
+    const stkb_map_desc saved = op.d;
+    int32_t lo[64], hi[64];
+    for (int i = 0; i < n_ranges; ++i) {  // clip to the map's own d0 box
+        lo[i] = int32_t(std::max<int64_t>(saved.lo[0], lo0[i]));
+        hi[i] = int32_t(std::min<int64_t>(saved.hi[0], hi0[i]));
+    }
+    int items = 0;
+    int rc = STKB_OK;
+    const bool streaming = op.d.kind != STKB_MAP_EXPR && dom->desc.ndim == 3;
+    if (streaming) {
+        RangeSpec rs;
+        rs.n = n_ranges;
+        rs.lo = lo;
+        rs.hi = hi;
+        rs.n_signal = n_signal;
+        rs.signal_items = &items;
+        rc = dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, rs)
+                                         : launch_star_map<double>(dom, op, dom->binding, rs);
+    } else {
+        // one launch per range; a stream-ordered marker after the signal ranges
+        int32_t* sig = dom->d_flags + kMaxTags + kMaxMaps + op.slot;
+        for (int i = 0; i < n_ranges && rc == STKB_OK; ++i) {
+            if (hi[i] > lo[i]) {
+                op.d.lo[0] = lo[i];
+                op.d.hi[0] = hi[i];
+                if (op.d.kind == STKB_MAP_EXPR) rc = launch_expr_map(dom, op, dom->binding);
+                else if (dom->desc.dtype == STKB_F32) rc = launch_star_map<float>(dom, op, dom->binding);
+                else rc = launch_star_map<double>(dom, op, dom->binding);
+            }
+            if (rc == STKB_OK && n_signal > 0 && i == n_signal - 1) {
+                cudaError_t e = launch_signal_add(sig, 1, dom->stream);
+                if (e != cudaSuccess) rc = fail(STKB_ERR_CUDA, cudaGetErrorString(e));
+                items = 1;
+            }
+        }
+        op.d = saved;
+    }
+    if (signal_items) *signal_items = items;
+    return rc;
+}
+
+int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, int32_t value) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
+    static PFN_cuStreamWaitValue32_v2 wait_fn = nullptr;
+    if (!wait_fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 entry point unavailable");
+        wait_fn = reinterpret_cast<PFN_cuStreamWaitValue32_v2>(fn);
+    }
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    int32_t* sig = dom->d_flags + kMaxTags + kMaxMaps + dom->maps[map_index].slot;
+    CUresult r = wait_fn(static_cast<CUstream>(stream ? stream : dom->stream), reinterpret_cast<CUdeviceptr>(sig),
+                         cuuint32_t(value), CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(int(r)));
+    return STKB_OK;
+}
+
+int stkb_set_max_ctas(stkb_domain* dom, int32_t ctas) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->ctas_override = std::max<int32_t>(0, ctas);
+    return STKB_OK;
 }
 
 int stkb_apply_swap(stkb_domain* dom, int32_t a, int32_t b) {

@@ -178,9 +178,12 @@ def localize(body: tuple, start: int, size: int) -> tuple:
 def run_step(eng, dist, group=None) -> None:
     """One time step of ``eng.body`` on this rank's slab.
 
-    ``eng`` provides launch(i, lo0, hi0), swap(a, b), view(grid, z0, planes),
-    and the overlap hooks boundary_done() / comm_context(token) / join(works);
-    the device engine maps them to CUDA streams, the CPU test engine to no-ops."""
+    ``eng`` provides launch(i, lo0, hi0), launch_with_boundary(i, r) (boundary
+    sub-slabs [0,r) and [n-r,n) computed first, then the interior; returns a
+    token for "boundary stored"), swap(a, b), view(grid, z0, planes) and the
+    overlap hooks comm_context(token) / join(works); the device engine maps
+    them to one kernel launch + a stream wait on the kernel's boundary signal,
+    the CPU test engine to sequential oracle calls."""
     plan = eng.plan
     n = plan.size
     for i, s in enumerate(eng.body):
@@ -192,18 +195,24 @@ def run_step(eng, dist, group=None) -> None:
             eng.launch(i, 0, n)
             continue
         r = max(ex.values())
-        # boundary planes first, then the exchange overlaps the interior
-        eng.launch(i, 0, min(r, n))
-        eng.launch(i, max(n - r, r), n)
-        token = eng.boundary_done()
+        token = eng.launch_with_boundary(i, r)
         views = {"_reach": ex}
         for g, reach in ex.items():
             for _, _, z, m in plan.messages(reach):
                 views[(g, z, m)] = eng.view(g, z, m)
         with eng.comm_context(token):
             works = exchange(dist, plan, views, group)
-        eng.launch(i, r, n - r)
         eng.join(works)
+
+
+def boundary_ranges(n: int, r: int) -> list:
+    """[(lo, hi)] of the two boundary sub-slabs then the interior (no overlaps)."""
+    lo_b = (0, min(r, n))
+    hi_b = (max(n - r, r), n)
+    out = [lo_b] + ([hi_b] if hi_b[1] > hi_b[0] else [])
+    if n - r > r:
+        out.append((r, n - r))
+    return out
 
 
 class DeviceSlabEngine:
@@ -238,6 +247,16 @@ class DeviceSlabEngine:
         self.dt.set_stream(self.compute.cuda_stream)
         self.tdtype = torch.float32 if d0.dtype == "f32" else torch.float64
         self.launches = 0
+        self.signal_target = {}  # map index -> running sum of its boundary signal
+        if plan.world > 1:
+            import os
+
+            from . import _lib as L
+
+            # leave SMs free so NCCL's copy kernels run while the interior computes
+            sms = torch.cuda.get_device_properties(device).multi_processor_count
+            reserve = int(os.environ.get("STKB_NCCL_SMS", "4"))
+            L.call("stkb_set_max_ctas", self.dt.h, max(1, sms - reserve))
 
     def view(self, name: str, z0: int, n: int):
         from . import _lib as L
@@ -265,13 +284,28 @@ class DeviceSlabEngine:
 
         L.call("stkb_apply_swap", self.dt.h, self.dt.index[a], self.dt.index[b])
 
-    def boundary_done(self):
-        ev = self.torch.cuda.Event()
-        ev.record(self.compute)
-        return ev
+    def launch_with_boundary(self, i: int, r: int):
+        """One launch: boundary items first (each bumps the map's signal), then the interior."""
+        from . import _lib as L
 
-    def comm_context(self, ev):
-        self.comm.wait_event(ev)
+        rng = boundary_ranges(self.plan.size, r)
+        lo = (ctypes.c_int64 * len(rng))(*[a for a, _ in rng])
+        hi = (ctypes.c_int64 * len(rng))(*[b for _, b in rng])
+        nsig = min(2, len(rng)) if len(rng) > 1 else 1
+        items = ctypes.c_int32()
+        k = self.map_index[i]
+        L.call("stkb_launch_map_ranges", self.dt.h, k, len(rng), lo, hi, nsig, ctypes.byref(items))
+        self.launches += 1
+        self.signal_target[k] = self.signal_target.get(k, 0) + items.value
+        return k, self.signal_target[k]
+
+    def comm_context(self, token):
+        from . import _lib as L
+
+        k, target = token
+        # the exchange stream waits (no SM held) until every boundary item is stored
+        L.call("stkb_stream_wait_signal", self.dt.h, ctypes.c_void_p(self.comm.cuda_stream), k,
+               ctypes.c_int32(target & 0x7FFFFFFF))
         return self.torch.cuda.stream(self.comm)
 
     def join(self, works) -> None:

@@ -42,6 +42,17 @@ def test_exchange_schedule_forms():
         assert sched[1] == {}
 
 
+def test_boundary_ranges_cover_the_slab_once():
+    from paper_2309_04671_b200.slabs import boundary_ranges
+
+    for n in (1, 3, 4, 7, 8, 9, 128):
+        for r in (1, 2, 4):
+            rng = boundary_ranges(n, r)
+            covered = sorted(z for lo, hi in rng for z in range(lo, hi))
+            assert covered == list(range(n)), (n, r, rng)
+            assert rng[0][0] == 0
+
+
 def test_messages_land_in_neighbour_halo():
     mid = SlabPlan(30, 3, 1, 4)
     assert mid.messages(4) == [("send", 0, 0, 4), ("recv", 0, -4, 4), ("send", 2, 6, 4), ("recv", 2, 10, 4)]
@@ -76,7 +87,11 @@ class CpuSlabEngine:
         per = int(np.prod(buf.data.shape[1:]))
         return flat[(z0 + o) * per:(z0 + o + n) * per]
 
-    def boundary_done(self):
+    def launch_with_boundary(self, i, r):
+        from paper_2309_04671_b200.slabs import boundary_ranges
+
+        for lo, hi in boundary_ranges(self.plan.size, r):
+            self.launch(i, lo, hi)
         return None
 
     def comm_context(self, _):

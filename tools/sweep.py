@@ -41,6 +41,9 @@ def time_one(builder, shape, dtype, steps=20, warm=3):
 
 
 if __name__ == "__main__":
+    import os
+
+    steps = int(os.environ.get("SWEEP_STEPS", "20"))
     for spec in sys.argv[1:]:
         b, s, d = spec.split(":")
-        print(json.dumps(time_one(b, tuple(int(x) for x in s.split(",")), d)), flush=True)
+        print(json.dumps(time_one(b, tuple(int(x) for x in s.split(",")), d, steps=steps)), flush=True)

@@ -256,7 +256,8 @@ def test_fast_vs_exact_one_step_at_full_size(builder):
     dst = [u.dest for u in bmap.kernel.updates][0]
     dst_grid = dict(bmap.grid_args)[dst]
     extra = dst_grid + "_x"
-    grids = {n: GridBuffer("f32", shape, decls[n].order, np.zeros((1, 1, 1), np.float32)) for n in names + [extra]}
+    order = decls[names[0]].order
+    grids = {n: GridBuffer("f32", shape, order, np.zeros((1, 1, 1), np.float32)) for n in names + [extra]}
     gen = torch.Generator(device="cuda").manual_seed(5)
     with DeviceTarget(grids, names + [extra], precision="fast") as fast:
         for n in names:

@@ -120,9 +120,17 @@ __device__ __forceinline__ void decode_item(const A& a, int item, int& tx, int& 
     const int per = a.n_tx * a.n_ty;
     tz = item / per;
     const int r = item - tz * per;
-    if (a.order_y_fast) {
+    if (a.order_y_fast == 1) {
         ty = r % a.n_ty;
         tx = r / a.n_ty;
+    } else if (a.order_y_fast >= 2) {
+        // bands of G tile rows: y fastest inside a band, then x, then the next band
+        const int G = a.order_y_fast;
+        const int band = r / (G * a.n_tx);
+        const int rb = r - band * G * a.n_tx;
+        const int rows = min(G, a.n_ty - band * G);
+        ty = band * G + rb % rows;
+        tx = rb / rows;
     } else {
         tx = r % a.n_tx;
         ty = r / a.n_tx;

@@ -234,6 +234,7 @@ class DeviceTarget:
 
     def run(self, steps: int) -> None:
         L.call("stkb_run", self.h, ctypes.c_int64(int(steps)))
+        self.total_launches = getattr(self, "total_launches", 0) + self.launches()
 
     def sync(self) -> None:
         L.call("stkb_sync", self.h)
@@ -312,18 +313,34 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
     # grids no map touches still take part in swaps: give them device slots too
     names = used + [n for n in grids if n not in used and _same_layout(grids[n], grids[used[0]])]
     out = {n: b.copy() for n, b in grids.items() if n not in names}
+    dead = dead_on_entry(bound.stmts, names, bindings or {})
+    h2d = d2h = 0
     with DeviceTarget({n: grids[n] for n in names}, names, device=device, precision=precision) as dt:
         for n in names:
+            # a fresh device grid is all zeros: an input whose interior is overwritten
+            # before anything reads it and whose halo is zero needs no transfer
+            if n in dead and halo_is_zero(grids[n]):
+                continue
             dt.upload(n, grids[n].data, sync=False)
+            h2d += grids[n].data.nbytes
         dt.sync()
         dt.execute(bound.stmts, bindings)
         for n in names:
             b = grids[n]
             arr = _host_array(b.data.shape, dt.np_dtype, pinned)
             dt.download(n, arr, sync=False)
+            d2h += arr.nbytes
             out[n] = type(b)(b.dtype, b.shape, b.order, arr)
         dt.sync()
+    LAST_RUN.update(h2d_bytes=h2d, d2h_bytes=d2h, launches=dt_launches(dt))
     return {n: out[n] for n in grids}
+
+
+LAST_RUN: dict = {}  # transfer accounting of the last run_gpu call (bench.py's e2e)
+
+
+def dt_launches(dt) -> int:
+    return getattr(dt, "total_launches", 0)
 
 
 def _host_array(shape, dtype, pinned: bool) -> np.ndarray:
@@ -333,6 +350,85 @@ def _host_array(shape, dtype, pinned: bool) -> np.ndarray:
 
     t = torch.empty(shape, dtype=torch.float32 if dtype == np.float32 else torch.float64, pin_memory=True)
     return t.numpy()
+
+
+def _reads_writes(bmap) -> tuple:
+    params = dict(bmap.grid_args)
+    reads, writes = set(), set()
+    kern = bmap.kernel
+    from .program import walk, node_kind
+
+    for e in [e for _, e in kern.locals] + [u.expr for u in kern.updates]:
+        for n in walk(e):
+            if node_kind(n) == "Read":
+                reads.add(params[n.grid])
+    for u in kern.updates:
+        if not any(u.offset):
+            writes.add(params[u.dest])
+    return reads, writes
+
+
+def _covers_interior(bmap, shape) -> bool:
+    from .matcher import map_box, MatchError
+
+    try:
+        box = map_box(bmap)
+    except MatchError:
+        return False
+    return tuple(box) == tuple((0, e) for e in shape)
+
+
+def dead_on_entry(stmts, names, bindings: dict, shape=None) -> set:
+    """Grid names whose input interior is never observed: the first access to
+    their buffer is a map that overwrites the whole interior without reading it
+    (executor.py semantics: every read sees pre-map values)."""
+    bufs = {n: n for n in names}  # name -> buffer identity
+    seen, dead = set(), set()
+
+    def visit(sts) -> bool:  # False = stop (unknown control flow)
+        for s in sts:
+            k = stmt_kind(s)
+            if k == "BoundSwap":
+                if s.first in bufs and s.second in bufs:
+                    bufs[s.first], bufs[s.second] = bufs[s.second], bufs[s.first]
+            elif k == "BoundFor":
+                count = s.count if isinstance(s.count, int) else bindings.get(s.count)
+                if count is None:
+                    return False
+                if int(count) > 0 and not visit(s.body):
+                    return False
+            elif k == "BoundMap":
+                reads, writes = _reads_writes(s)
+                full = _covers_interior(s, s.info.dest_extents or ()) if s.info.dest_extents else False
+                for g in reads:
+                    if g in bufs:
+                        seen.add(bufs[g])
+                for g in writes:
+                    if g in bufs and bufs[g] not in seen:
+                        seen.add(bufs[g])
+                        if full:
+                            dead.add(bufs[g])
+            if len(seen) == len(bufs):
+                return False
+        return True
+
+    visit(stmts)
+    return dead
+
+
+def halo_is_zero(g) -> bool:
+    d, o = g.data, g.order
+    if o == 0:
+        return True
+    nd = d.ndim
+    for ax in range(nd):
+        lo = [slice(None)] * nd
+        hi = [slice(None)] * nd
+        lo[ax] = slice(0, o)
+        hi[ax] = slice(d.shape[ax] - o, d.shape[ax])
+        if d[tuple(lo)].any() or d[tuple(hi)].any():
+            return False
+    return True
 
 
 def _same_layout(a, b) -> bool:

@@ -9,6 +9,8 @@
 // Any kernel the reference accepts (star, box, "other", locals, scalars,
 // several updates, 2-D) runs here; the tuned streaming kernels cover the star
 // forms at HBM speed.
+#include <algorithm>
+
 #include "common.cuh"
 #include "../../include/stkb200.h"
 
@@ -169,6 +171,27 @@ cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const 
 }
 
 size_t compare_partial_bytes() { return sizeof(ComparePartial); }
+
+// copy `nrows` rows of `row_words` 32-bit words between two row pitches
+// (the unpitched GridBuffer layout <-> the 128-byte pitched device layout)
+__global__ void __launch_bounds__(256) repitch_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                      int64_t nrows, int64_t row_words, int64_t src_pitch,
+                                                      int64_t dst_pitch) {
+    for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const uint32_t* s = src + r * src_pitch;
+        uint32_t* d = dst + r * dst_pitch;
+        for (int64_t i = threadIdx.x; i < row_words; i += blockDim.x) d[i] = s[i];
+    }
+}
+
+cudaError_t launch_repitch(const void* src, void* dst, int64_t nrows, int64_t row_bytes, int64_t src_pitch_bytes,
+                           int64_t dst_pitch_bytes, int num_sms, cudaStream_t s) {
+    if (nrows <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>(nrows, int64_t(num_sms) * 16);
+    repitch_kernel<<<int(blocks), 256, 0, s>>>(static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), nrows,
+                                               row_bytes / 4, src_pitch_bytes / 4, dst_pitch_bytes / 4);
+    return cudaGetLastError();
+}
 
 __global__ void signal_add_kernel(int32_t* p, int32_t v) {
     __threadfence();

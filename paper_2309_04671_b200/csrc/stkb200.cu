@@ -28,6 +28,8 @@ cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const 
                            int blocks, cudaStream_t s);
 size_t compare_partial_bytes();
 cudaError_t launch_signal_add(int32_t* p, int32_t v, cudaStream_t s);
+cudaError_t launch_repitch(const void* src, void* dst, int64_t nrows, int64_t row_bytes, int64_t src_pitch_bytes,
+                           int64_t dst_pitch_bytes, int num_sms, cudaStream_t s);
 struct Star2DArgs {
     int64_t pitch;
     int64_t lead;
@@ -118,6 +120,8 @@ struct stkb_domain {
     int64_t last_launches = 0;
     int32_t* d_flags = nullptr;
     void* d_partials = nullptr;
+    void* d_stage = nullptr;  // H2D staging: contiguous PCIe copies, then a repitch kernel
+    size_t stage_bytes = 0;
     int lz_override = 0;
     int ctas_override = 0;
     int l2promo = 3;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
@@ -419,6 +423,7 @@ int stkb_domain_destroy(stkb_domain* dom) {
     for (void* b : dom->snap) if (b) cudaFree(b);
     if (dom->d_flags) cudaFree(dom->d_flags);
     if (dom->d_partials) cudaFree(dom->d_partials);
+    if (dom->d_stage) cudaFree(dom->d_stage);
     if (dom->ev0) cudaEventDestroy(dom->ev0);
     if (dom->ev1) cudaEventDestroy(dom->ev1);
     if (dom->own_stream) cudaStreamDestroy(dom->own_stream);
@@ -454,10 +459,31 @@ static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     const Geometry& g = dom->g;
     const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
+    const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
     char* dst = static_cast<char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
-    CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(g.pitch) * dom->elem, host, row, row,
-                               size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order), cudaMemcpyHostToDevice,
-                               dom->stream));
+    // A pitched cudaMemcpy2D runs at ~60 % of PCIe speed on B200 hosts; copy
+    // contiguous chunks into a staging buffer instead and repitch on the device.
+    constexpr size_t kStage = size_t(256) << 20;
+    if (!dom->d_stage) {
+        dom->stage_bytes = std::min(kStage, rows * row);
+        if (cudaMalloc(&dom->d_stage, dom->stage_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            dom->d_stage = nullptr;
+        }
+    }
+    if (!dom->d_stage) {  // no memory for staging: direct pitched copy
+        CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(g.pitch) * dom->elem, host, row, row, rows, cudaMemcpyHostToDevice,
+                                   dom->stream));
+        return STKB_OK;
+    }
+    const size_t chunk_rows = std::max<size_t>(1, dom->stage_bytes / row);
+    const char* src = static_cast<const char*>(host);
+    for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+        const size_t nr = std::min(chunk_rows, rows - r0);
+        CUDA_TRY(cudaMemcpyAsync(dom->d_stage, src + r0 * row, nr * row, cudaMemcpyHostToDevice, dom->stream));
+        CUDA_TRY(launch_repitch(dom->d_stage, dst + r0 * size_t(g.pitch) * dom->elem, int64_t(nr), int64_t(row),
+                                int64_t(row), int64_t(g.pitch) * int64_t(dom->elem), dom->num_sms, dom->stream));
+    }
     return STKB_OK;
 }
 

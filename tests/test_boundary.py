@@ -175,3 +175,21 @@ def test_plan_gpu_mirrors_reference_rules():
     bound, _ = corpus.config_target("star3d4r", (16, 16, 18), 1)
     with pytest.raises(PlanError, match="divisible by 4"):
         plan_gpu(next(_maps(bound.stmts)).info, {"template": "f4"})
+
+
+def test_dead_inputs_detected():
+    from paper_2309_04671_b200.backend import dead_on_entry, halo_is_zero
+    from paper_2309_04671_b200.grids import GridBuffer
+
+    for builder, expect in (("star3d4r", {"v"}), ("wave", set()), ("j3d27pt", {"v"}), ("star2d4r", {"v"})):
+        shape = (16, 16) if builder.startswith("star2d") else (16, 16, 16)
+        bound, decls = corpus.config_target(builder, shape, 3)
+        assert dead_on_entry(bound.stmts, list(decls), {}) == expect, builder
+    bound, decls = corpus.config_target("star3d4r", (16, 16, 16), "n")
+    assert dead_on_entry(bound.stmts, list(decls), {}) == set()  # unknown loop bound: conservative
+    assert dead_on_entry(bound.stmts, list(decls), {"n": 0}) == set()  # the body never runs
+    g = GridBuffer.zeros((4, 5, 6), 2)
+    g.interior[...] = 1.0
+    assert halo_is_zero(g)
+    g.data[0, 3, 3] = 1.0
+    assert not halo_is_zero(g)

@@ -292,3 +292,25 @@ def test_fast_vs_exact_one_step_at_full_size(builder):
                ctypes.byref(w), ctypes.byref(sc))
         assert sc.value > 0
         assert me.value / sc.value <= 1e-6, (me.value, sc.value, w.value)
+
+
+@pytest.mark.parametrize("v_halo", [0.0, 3.5])
+def test_dead_input_skip_keeps_semantics(v_halo):
+    """v's interior is dead on entry (overwritten by the first map); its halo is
+    live (read after the first swap).  Garbage interior must not matter; a
+    non-zero halo must be uploaded."""
+    from paper_2309_04671_b200.backend import LAST_RUN
+
+    bound, decls = corpus.config_target("star3d2r", (20, 24, 40), 3)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 8)
+    grids["v"].interior[...] = 12345.0
+    if v_halo:
+        grids["v"].data[0, :, :] = v_halo
+        grids["v"].data[:, :, -1] = v_halo
+    ref = oracle.run_target_c(bound, grids)
+    got = run_gpu(bound, _plan(bound), grids, precision="exact")
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), n
+    nbytes = grids["u"].data.nbytes
+    assert LAST_RUN["h2d_bytes"] == (2 * nbytes if v_halo else nbytes)

@@ -206,6 +206,7 @@ def run_ours(args) -> None:
     peaks = measured_peaks()
     npts = int(np.prod(shape))
 
+    slab_e2e = None
     if ws == 1 and not args.force_slabs:
         bound, decls = corpus.config_target(builder, shape, K, dtype)
         names = list(decls)
@@ -238,6 +239,15 @@ def run_ours(args) -> None:
         local_pts = sb.local_points
         comm = sb.comm_info()
         sb.close()
+        if not args.no_e2e:
+            from paper_2309_04671_b200.slabs import slab_e2e
+
+            e = slab_e2e(builder, shape, dtype, K, sb.plan, sb.dist, local)
+            slab_e2e = {"value": npts * K / e["seconds"] / 1e9, "unit": "GPts/s",
+                        "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
+                        "steps_per_call": K, "seconds": e["seconds"],
+                        "what": "slabs.run_slab per rank: H2D of the rank's slabs from pinned host memory, "
+                                f"{K} steps with NCCL halo exchange, D2H; wall clock, max over ranks"}
     if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
@@ -250,7 +260,7 @@ def run_ours(args) -> None:
     achieved = local_pts * bpp / (sec / K) / 1e9  # per-GPU algorithmic GB/s of the dominant kernel
 
     # ------------------------------------------------------------ end to end
-    e2e = None
+    e2e = slab_e2e if (ws > 1 or args.force_slabs) and not args.no_e2e else None
     if not args.no_e2e and ws == 1 and not args.force_slabs:
         bound, decls = corpus.config_target(builder, shape, K, dtype)
         grids = pinned_grids(decls, builder)

@@ -321,6 +321,94 @@ class DeviceSlabEngine:
         self.dt.close()
 
 
+def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Optional[int] = None,
+             precision: str = "fast", bindings: Optional[dict] = None, pinned: bool = False) -> dict:
+    """Multi-GPU counterpart of :func:`paper_2309_04671_b200.run_gpu` (one call per rank).
+
+    ``local_grids`` are this rank's slabs: GridBuffers of shape
+    ``(slab.size, n1, n2)`` whose data is the global padded array sliced with
+    ``slab.global_slice()`` (d0 halo planes included).  The target must be a
+    ``for`` loop over maps and swaps; every step runs :func:`run_step` (boundary
+    items first, halo exchange over ``dist`` overlapped with the interior).
+    Returns this rank's slabs after the loop, in host memory."""
+    from .backend import ExecutionError, _host_array, check_plan, default_device
+
+    check_plan(plan, bound)
+    loops = [s for s in bound.stmts if stmt_kind(s) == "BoundFor"]
+    if len(bound.stmts) != 1 or not loops:
+        raise ExecutionError("run_slab runs targets of the form `for _ in range(n): maps and swaps`")
+    loop = loops[0]
+    count = loop.count if isinstance(loop.count, int) else int((bindings or {})[loop.count])
+    names = list(local_grids)
+    glob = {n: _Decl(g, slab) for n, g in local_grids.items()}
+    eng = DeviceSlabEngine(tuple(loop.body), glob, slab, default_device() if device is None else device, precision)
+    try:
+        for n in names:
+            eng.dt.upload(n, local_grids[n].data, sync=False)
+        eng.dt.sync()
+        for _ in range(count):
+            eng.step(dist)
+        eng.torch.cuda.synchronize()
+        out = {}
+        for n in names:
+            b = local_grids[n]
+            arr = _host_array(b.data.shape, eng.dt.np_dtype, pinned)
+            eng.dt.download(n, arr, sync=False)
+            out[n] = type(b)(b.dtype, tuple(b.shape), b.order, arr)
+        eng.dt.sync()
+        return out
+    finally:
+        eng.close()
+
+
+class _Decl:
+    """Declaration view of a (local) GridBuffer; with a SlabPlan, the global one."""
+
+    def __init__(self, g, slab: Optional[SlabPlan] = None):
+        self.dtype, self.order = g.dtype, g.order
+        shape = tuple(g.shape)
+        self.shape = (slab.n0,) + shape[1:] if slab is not None else shape
+
+
+def slab_e2e(builder: str, shape, dtype: str, k: int, slab: SlabPlan, dist, device: int) -> dict:
+    """bench.py's N>1 e2e: run_slab on this rank's slabs from pinned host memory, k steps, back;
+    wall clock, max over ranks."""
+    import time
+
+    import torch
+
+    from . import corpus
+    from .grids import GridBuffer
+    from .planning import plan_gpu
+
+    bound, decls = corpus.config_target(builder, shape, k, dtype)
+    local_shape = (slab.size,) + tuple(shape[1:])
+    grids = {}
+    for n, d in decls.items():
+        padded = tuple(e + 2 * d.order for e in local_shape)
+        t = torch.zeros(padded, dtype=torch.float32 if dtype == "f32" else torch.float64, pin_memory=True)
+        grids[n] = GridBuffer(dtype, local_shape, d.order, t.numpy())
+    first = next(iter(grids.values()))
+    rng = np.random.default_rng(7 + slab.rank)
+    inner = first.interior
+    for z in range(inner.shape[0]):
+        inner[z] = (10.0 ** rng.uniform(-4.0, 5.0, size=inner.shape[1:])).astype(inner.dtype)
+    if builder == "wave":
+        grids["kap"].interior[...] = 0.01
+        grids["up"].data[...] = first.data
+    bmap = next(s for s in bound.stmts[0].body if stmt_kind(s) == "BoundMap")
+    plan = plan_gpu(bmap.info, {"template": "unroll", "computeCapability": "10.0"})
+    dist.barrier()
+    t0 = time.perf_counter()
+    out = run_slab(bound, plan, grids, slab, dist, device=device, pinned=True)
+    sec = time.perf_counter() - t0
+    t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nbytes = sum(g.data.nbytes for g in grids.values())
+    del out
+    return {"seconds": float(t.item()), "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+
+
 class SlabBench:
     """bench.py's N>1 path: strong scaling of one configuration over z-slabs."""
 

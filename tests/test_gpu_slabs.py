@@ -109,3 +109,19 @@ def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precisi
             assert compare(ref[n], got).max_relative <= 1e-5, (n, compare(ref[n], got).render())
     for eng in engines:
         eng.close()
+
+
+def test_run_slab_single_rank_matches_run_gpu():
+    from paper_2309_04671_b200 import run_gpu
+    from paper_2309_04671_b200.planning import plan_gpu
+    from paper_2309_04671_b200.slabs import run_slab
+
+    bound, decls, grids = _case("star3d4r_norm", (36, 40, 72), 5)
+    bmap = bound.stmts[0].body[0]
+    plan = plan_gpu(bmap.info, {"template": "unroll", "computeCapability": "10.0"})
+    slab = SlabPlan(36, 1, 0, 4)
+    local = {n: GridBuffer(g.dtype, tuple(g.shape), g.order, g.data[slab.global_slice()].copy()) for n, g in grids.items()}
+    got = run_slab(bound, plan, local, slab, dist=None, device=0)
+    ref = run_gpu(bound, plan, grids, device=0)
+    for n in grids:
+        assert np.array_equal(got[n].data, ref[n].data), n

@@ -331,7 +331,7 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
     ``for`` loop over maps and swaps; every step runs :func:`run_step` (boundary
     items first, halo exchange over ``dist`` overlapped with the interior).
     Returns this rank's slabs after the loop, in host memory."""
-    from .backend import ExecutionError, _host_array, check_plan, default_device
+    from .backend import ExecutionError, _host_array, check_plan, dead_on_entry, default_device, halo_is_zero
 
     check_plan(plan, bound)
     loops = [s for s in bound.stmts if stmt_kind(s) == "BoundFor"]
@@ -342,8 +342,11 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
     names = list(local_grids)
     glob = {n: _Decl(g, slab) for n, g in local_grids.items()}
     eng = DeviceSlabEngine(tuple(loop.body), glob, slab, default_device() if device is None else device, precision)
+    dead = dead_on_entry(bound.stmts, names, bindings or {})
     try:
         for n in names:
+            if n in dead and halo_is_zero(local_grids[n]):
+                continue  # fresh device grids are zero; this input is never observed
             eng.dt.upload(n, local_grids[n].data, sync=False)
         eng.dt.sync()
         for _ in range(count):
@@ -398,15 +401,21 @@ def slab_e2e(builder: str, shape, dtype: str, k: int, slab: SlabPlan, dist, devi
         grids["up"].data[...] = first.data
     bmap = next(s for s in bound.stmts[0].body if stmt_kind(s) == "BoundMap")
     plan = plan_gpu(bmap.info, {"template": "unroll", "computeCapability": "10.0"})
+    run_slab(bound, plan, grids, slab, dist, device=device, pinned=True)  # warm: context, pinned pool
+    torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     out = run_slab(bound, plan, grids, slab, dist, device=device, pinned=True)
     sec = time.perf_counter() - t0
     t = torch.tensor([sec], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    nbytes = sum(g.data.nbytes for g in grids.values())
+    from .backend import dead_on_entry, halo_is_zero
+
+    dead = dead_on_entry(bound.stmts, list(grids), {})
+    h2d = sum(g.data.nbytes for n, g in grids.items() if not (n in dead and halo_is_zero(g)))
+    d2h = sum(g.data.nbytes for g in out.values())
     del out
-    return {"seconds": float(t.item()), "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+    return {"seconds": float(t.item()), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
 
 class SlabBench:

@@ -65,11 +65,25 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
 #pragma unroll
         for (int i = 0; i < NPK; ++i) acc[k][i] = K::mul(T(0), P{});
     P chk = K::mul(T(0), P{});
-    T nx[VEC + 2 * RA];  // prefetched next row: left halo | centre | right halo
-    {
-        const T* nrow = row0 + int64_t(z0 - R + a.order) * a.pitch;  // first row (a warm-up row: centre only)
-        ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&nx[RA]));
-    }
+    // rows in flight: a ring of D prefetched rows (left halo | centre | right halo);
+    // D divides the unroll factor NS so ring slots stay static registers
+    constexpr int D = 1;  // deeper rings (D = 3) cost occupancy and measured slower
+    T nx[D][VEC + 2 * RA];
+    auto fetch = [&](int qi_, T* dst) {
+        const int q_ = z0 - R + qi_;
+        const T* nrow = row0 + int64_t(q_ + a.order) * a.pitch;
+        ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&dst[RA]));
+        if (q_ >= z0 && q_ < z1) {
+#pragma unroll
+            for (int k = 0; k < RA / VEC; ++k) {
+                ldg16(nrow - RA + k * VEC, *reinterpret_cast<T(*)[VEC]>(&dst[k * VEC]));
+                ldg16(nrow + VEC + k * VEC, *reinterpret_cast<T(*)[VEC]>(&dst[RA + VEC + k * VEC]));
+            }
+        }
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (d < nq) fetch(d, nx[d]);
 
     for (int qb = 0; qb < nq; qb += NS) {
 #pragma unroll
@@ -77,21 +91,11 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
             const int qi = qb + p;
             if (qi >= nq) break;
             const int q = z0 - R + qi;
-            // this row was fetched one step ahead (nx); fetch the next one now
+            // this row was fetched D steps ahead; refill its ring slot with row qi + D
             T xr[VEC + 2 * RA];
 #pragma unroll
-            for (int i = 0; i < VEC + 2 * RA; ++i) xr[i] = nx[i];
-            if (qi + 1 < nq) {
-                const T* nrow = row0 + int64_t(q + 1 + a.order) * a.pitch;
-                ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&nx[RA]));
-                if (q + 1 >= z0 && q + 1 < z1) {
-#pragma unroll
-                    for (int k = 0; k < RA / VEC; ++k) {
-                        ldg16(nrow - RA + k * VEC, *reinterpret_cast<T(*)[VEC]>(&nx[k * VEC]));
-                        ldg16(nrow + VEC + k * VEC, *reinterpret_cast<T(*)[VEC]>(&nx[RA + VEC + k * VEC]));
-                    }
-                }
-            }
+            for (int i = 0; i < VEC + 2 * RA; ++i) xr[i] = nx[p % D][i];
+            if (qi + D < nq) fetch(qi + D, nx[p % D]);
             P cv[NPK];
 #pragma unroll
             for (int k = 0; k < NPK; ++k) cv[k] = K::make(&xr[RA + k * W]);

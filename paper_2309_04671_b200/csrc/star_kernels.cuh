@@ -45,7 +45,11 @@ struct StarCfg {
     static constexpr int HALO_ELEMS = ((HALO_ELEMS_RAW * int(sizeof(T)) + 127) / 128) * 128 / int(sizeof(T));
     static constexpr int CTR_ELEMS = BX * BY;
     static constexpr int STAGE_ELEMS = HALO_ELEMS + (FORM == FORM_WAVE ? 3 * CTR_ELEMS : 0);
+#ifdef STKB_EXP_NOYHALO
+    static constexpr uint32_t HALO_BYTES = SW * BY * sizeof(T);  // experiment: no y-halo rows loaded
+#else
     static constexpr uint32_t HALO_BYTES = HALO_ELEMS_RAW * sizeof(T);  // bytes the TMA delivers
+#endif
     static constexpr uint32_t CTR_BYTES = CTR_ELEMS * sizeof(T);
     static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * sizeof(T);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;

@@ -235,7 +235,11 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     int bx, by, hx;
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
+#ifdef STKB_EXP_NOYHALO
+    int rc = encode_map(dom, sb, bx + 2 * hx, by, &m_halo);
+#else
     int rc = encode_map(dom, sb, bx + 2 * hx, by + 2 * R, &m_halo);
+#endif
     if (rc) return rc;
     CUtensorMap maps[4];
     maps[0] = *m_halo;

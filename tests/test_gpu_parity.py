@@ -314,3 +314,29 @@ def test_dead_input_skip_keeps_semantics(v_halo):
         assert np.array_equal(ref[n].data, got[n].data), n
     nbytes = grids["u"].data.nbytes
     assert LAST_RUN["h2d_bytes"] == (2 * nbytes if v_halo else nbytes)
+
+
+def test_fast_path_is_deterministic_across_runs():
+    """The dynamic tile scheduler changes which CTA computes a tile, never the
+    per-point operation order: two runs are bit-identical."""
+    bound, decls = corpus.config_target("star3d4r_norm", (96, 90, 260), 7)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 12)
+    a = run_gpu(bound, _plan(bound), grids)
+    b = run_gpu(bound, _plan(bound), grids)
+    for n in a:
+        assert np.array_equal(a[n].data, b[n].data), n
+
+
+def test_fast_path_linearity_within_4ulp():
+    """test_executor.py:115-125 on the device path: out(2u) vs 2*out(u), one step."""
+    bound, decls = corpus.config_target("star3d4r", (40, 44, 72), 1)
+    g1 = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(g1["u"], 9)
+    g2 = {n: GridBuffer(b.dtype, b.shape, b.order, b.data * np.float32(2.0)) for n, b in g1.items()}
+    o1 = run_gpu(bound, _plan(bound), g1)
+    o2 = run_gpu(bound, _plan(bound), g2)
+    a = o1["u"].interior.astype(np.float64) * 2.0
+    b = o2["u"].interior.astype(np.float64)
+    rel = np.abs(a - b) / np.maximum(np.abs(a), np.finfo(np.float32).tiny)
+    assert rel.max() <= 4 * np.finfo(np.float32).eps

@@ -251,10 +251,13 @@ def analyze_kernel(kernel, grids: Optional[dict] = None) -> StencilInfo:
 
 
 def map_spec(extents: Sequence[int], width: int = 0) -> tuple:
-    """``map(e=extents[, w=width])`` -> per-dim (a0, a1, a2, a3) (analysis.py:322-330)."""
-    if width:
-        return tuple((0, width, e - width, e) for e in extents)
-    return tuple((0, 0, e, e) for e in extents)
+    """``map(e=extents[, w=width])`` -> per-dim (a0, a1, a2, a3), validated as
+    MapSpec.concrete does (analysis.py:133-160)."""
+    spec = tuple((0, width, e - width, e) for e in extents) if width else tuple((0, 0, e, e) for e in extents)
+    for axis, (a0, a1, a2, a3) in enumerate(spec):
+        if not (0 <= a0 <= a1 and a2 <= a3) or a1 > a3 or a2 < a0:
+            raise AnalysisError(f"map bounds for dimension {'ijk'[axis]} are out of order: {(a0, a1, a2, a3)}")
+    return spec
 
 
 SCHEMES = ("unified", "cross_product", "slab7")

@@ -202,6 +202,8 @@ def run_ours(args) -> None:
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     builder, shape, dtype, bpp, ref_name = CONFIGS[args.config]
+    if args.scaling == "weak":  # c4 weak scaling: (1024*G) x 1024 x 1024, fixed work per GPU
+        shape = (shape[0] * ws,) + tuple(shape[1:])
     K, W = args.steps, args.warmup
     peaks = measured_peaks()
     npts = int(np.prod(shape))
@@ -306,7 +308,7 @@ def run_ours(args) -> None:
             "warmup": W,
             "ms_per_step": round(per_step_ms, 4),
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32" if dtype == "f32" else "f64",
             "data": "synthetic (log-uniform [1e-4,1e5] interior, zero halo; generated on device)",
@@ -378,6 +380,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's grid split over N GPUs; weak: d0 grows with N")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -43,7 +43,10 @@ class NullDist:
 def main():
     cfg, world = sys.argv[1], int(sys.argv[2])
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+    weak = len(sys.argv) > 4 and sys.argv[4] == "weak"
     builder, shape, dtype, bpp, _ = bench.CONFIGS[cfg]
+    if weak:
+        shape = (shape[0] * world,) + tuple(shape[1:])
     bound, decls = corpus.config_target(builder, shape, 1, dtype)
     body = bound.stmts[0].body
     order = next(iter(decls.values())).order
@@ -64,7 +67,7 @@ def main():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
     pts = plan.size * shape[1] * shape[2]
-    print(json.dumps({"config": cfg, "world": world, "rank": rank, "slab_planes": plan.size, "ms_per_step": round(ms, 4),
+    print(json.dumps({"config": cfg, "scaling": "weak" if weak else "strong", "world": world, "rank": rank, "slab_planes": plan.size, "ms_per_step": round(ms, 4),
                       "rank_gpts": round(pts / ms / 1e6, 1), "implied_job_gpts": round(pts * world / ms / 1e6, 1)}))
     eng.close()
 

@@ -163,6 +163,31 @@ int stkb_launch_map_ranges(stkb_domain *dom, int32_t map_index, int32_t n_ranges
                            const int64_t *hi0, int32_t n_signal, int32_t *signal_items);
 int stkb_stream_wait_signal(stkb_domain *dom, void *stream, int32_t map_index, int32_t value);
 int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (leave SMs for NCCL) */
+
+/* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process
+ * per GPU).  Each rank exports its buffers and its 2-slot step-flag array with
+ * CUDA IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and
+ * registers them with stkb_set_peer (side 0 = lower neighbour, rank-1; side 1 =
+ * upper, rank+1; buffer i of the neighbour pairs with my buffer i).
+ * stkb_launch_map_push runs a map over its whole box and ALSO stores its first
+ * / last `push_planes` output planes into the neighbours' halo planes from the
+ * same kernel (peer-mapped st.global).  Ranks count their pushing launches;
+ * launch c is bracketed by stkb_peer_wait(c-1) (both neighbours finished
+ * launch c-1: their pushes into my halo are visible and they no longer read
+ * the halo I will overwrite) and stkb_peer_signal(c) (a fenced stream write
+ * into each neighbour's flag) — stream memory operations only: no kernel
+ * ever waits on another.  This replaces the NCCL send/recv of the halo
+ * planes (slabs.py run_step) for 3-D streaming maps. */
+int stkb_launch_map_push(stkb_domain *dom, int32_t map_index, int32_t push_planes);
+int stkb_buffer_ipc_handle(stkb_domain *dom, int32_t buffer, void *handle64);
+int stkb_flags_ipc_handle(stkb_domain *dom, void *handle64);
+int stkb_buffer_ptr(stkb_domain *dom, int32_t buffer, void **dptr);
+int stkb_flags_ptr(stkb_domain *dom, void **dptr);
+int stkb_ipc_open(int32_t device, const void *handle64, void **dptr);
+int stkb_ipc_close(int32_t device, void *dptr);
+int stkb_set_peer(stkb_domain *dom, int32_t side, int32_t n_bufs, void *const *bufs, void *flags, int64_t peer_n0);
+int stkb_peer_signal(stkb_domain *dom, void *stream, int32_t value);
+int stkb_peer_wait(stkb_domain *dom, void *stream, int32_t value);
 int stkb_apply_swap(stkb_domain *dom, int32_t a, int32_t b);
 int stkb_plane_span(stkb_domain *dom, int32_t name, int64_t z0, int64_t nplanes, void **dptr,
                     int64_t *bytes);

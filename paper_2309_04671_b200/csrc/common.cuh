@@ -56,6 +56,13 @@ struct StarArgs {
     T cb[125];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 2
     int32_t store_hint;        // 1: streaming (evict-first) output stores
     int32_t order_y_fast;      // work items walk y tiles fastest
+    // fused halo push (multi-GPU z-slabs): output planes z < push_planes are also
+    // stored into the lower neighbour's top halo (its plane push_lo_n0 + z), planes
+    // z >= n0 - push_planes into the upper neighbour's bottom halo (plane z - n0)
+    T* push_lo;
+    T* push_hi;
+    int64_t push_lo_n0;
+    int32_t push_planes;
 };
 
 // ---------------------------------------------------------------------------

@@ -483,6 +483,32 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                                         outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2, a.box.hi2);
                             }
                         }
+                        if (a.push_planes > 0) {
+                            // fused halo exchange: the boundary planes go straight into the
+                            // neighbours' halo planes over NVLink (peer-mapped stores)
+#pragma unroll
+                            for (int side = 0; side < 2; ++side) {
+                                T* pbase = side == 0 ? a.push_lo : a.push_hi;
+                                const bool hit = side == 0 ? (z < a.push_planes) : (z >= a.g.n0 - a.push_planes);
+                                if (pbase != nullptr && hit) {
+                                    const int64_t zp = side == 0 ? z + a.push_lo_n0 : int64_t(z) - a.g.n0;
+                                    T* const pz = pbase + (dst0 - a.dst) + (zp + a.g.order0) * plane;
+                                    if (full_tile) {
+#pragma unroll
+                                        for (int j = 0; j < TY; ++j) stg16(pz + j * pitch, outv[j]);
+                                    } else if (x_any) {
+#pragma unroll
+                                        for (int j = 0; j < TY; ++j) {
+                                            const int y = y0 + jr0 + j;
+                                            if (y >= a.box.lo1 && y < a.box.hi1)
+                                                store_row_masked<T>(pz + j * pitch, outv[j][0], outv[j][1 % VEC],
+                                                                    outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2,
+                                                                    a.box.hi2);
+                                        }
+                                    }
+                                }
+                            }
+                        }
                     }
                 }
             }

@@ -121,6 +121,14 @@ struct stkb_domain {
     int32_t* d_flags = nullptr;
     void* d_partials = nullptr;
     void* d_stage = nullptr;  // H2D staging: contiguous PCIe copies, then a repitch kernel
+    // z-slab neighbours for the fused halo push: [0] lower (rank-1), [1] upper (rank+1)
+    struct Peer {
+        bool set = false;
+        std::vector<void*> bufs;  // the neighbour's buffer i (same binding history on every rank)
+        int32_t* flags = nullptr; // the neighbour's step flags ([0] from its lower, [1] from its upper)
+        int64_t n0 = 0;           // the neighbour's slab thickness
+    } peer[2];
+    int32_t* d_peer_flags = nullptr;  // my step flags: [0] written by my lower, [1] by my upper neighbour
     size_t stage_bytes = 0;
     int lz_override = 0;
     int ctas_override = 0;
@@ -202,7 +210,7 @@ struct RangeSpec {
 
 template <typename T>
 int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind,
-                    const RangeSpec& rs = RangeSpec()) {
+                    const RangeSpec& rs = RangeSpec(), int push_planes = 0) {
     const stkb_map_desc& d = op.d;
     if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
     StarArgs<T> a{};
@@ -229,6 +237,13 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.wave_b = T(d.wave_b);
     a.store_hint = dom->store_hint;
     a.order_y_fast = dom->order_y_fast;
+    if (push_planes > 0) {
+        const int db = bind[d.dst];
+        a.push_planes = push_planes;
+        a.push_lo = dom->peer[0].set ? static_cast<T*>(dom->peer[0].bufs[db]) : nullptr;
+        a.push_hi = dom->peer[1].set ? static_cast<T*>(dom->peer[1].bufs[db]) : nullptr;
+        a.push_lo_n0 = dom->peer[0].n0;
+    }
     if (d.kind == STKB_MAP_BOX)
         for (int i = 0; i < 125; ++i) a.cb[i] = T(d.box_coef[i]);
 
@@ -404,6 +419,8 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     // per map; then one boundary-signal counter per map (slab halo exchange)
     if (cudaMalloc(&dom->d_flags, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
     cudaMemset(dom->d_flags, 0, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t));
+    if (cudaMalloc(&dom->d_peer_flags, 2 * sizeof(int32_t)) != cudaSuccess) return cleanup("peer flags");
+    cudaMemset(dom->d_peer_flags, 0, 2 * sizeof(int32_t));
     if (const char* s = getenv("STKB_LZ")) dom->lz_override = atoi(s);
     if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
     if (const char* s = getenv("STKB_L2PROMO")) dom->l2promo = atoi(s);
@@ -428,6 +445,7 @@ int stkb_domain_destroy(stkb_domain* dom) {
     if (dom->d_flags) cudaFree(dom->d_flags);
     if (dom->d_partials) cudaFree(dom->d_partials);
     if (dom->d_stage) cudaFree(dom->d_stage);
+    if (dom->d_peer_flags) cudaFree(dom->d_peer_flags);
     if (dom->ev0) cudaEventDestroy(dom->ev0);
     if (dom->ev1) cudaEventDestroy(dom->ev1);
     if (dom->own_stream) cudaStreamDestroy(dom->own_stream);
@@ -829,17 +847,137 @@ int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges
     return rc;
 }
 
+int stkb_launch_map_push(stkb_domain* dom, int32_t map_index, int32_t push_planes) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
+    MapOp& op = dom->maps[map_index];
+    if (op.d.kind == STKB_MAP_EXPR || dom->desc.ndim != 3)
+        return fail(STKB_ERR_UNSUPPORTED, "the fused halo push needs a 3-D streaming map");
+    if (push_planes < 0 || push_planes > dom->g.order0 || push_planes > dom->g.n0)
+        return fail(STKB_ERR_ARG, "push_planes must be in 0..min(order, n0)");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    return dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, RangeSpec(), push_planes)
+                                       : launch_star_map<double>(dom, op, dom->binding, RangeSpec(), push_planes);
+}
+
+int stkb_buffer_ipc_handle(stkb_domain* dom, int32_t buffer, void* handle) {
+    if (!dom || !handle) return fail(STKB_ERR_ARG, "null argument");
+    if (buffer < 0 || buffer >= dom->desc.n_grids) return fail(STKB_ERR_ARG, "buffer index out of range");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, dom->bufs[buffer]));
+    memcpy(handle, &h, sizeof(h));
+    return STKB_OK;
+}
+
+int stkb_flags_ipc_handle(stkb_domain* dom, void* handle) {
+    if (!dom || !handle) return fail(STKB_ERR_ARG, "null argument");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, dom->d_peer_flags));
+    memcpy(handle, &h, sizeof(h));
+    return STKB_OK;
+}
+
+int stkb_flags_ptr(stkb_domain* dom, void** dptr) {
+    if (!dom || !dptr) return fail(STKB_ERR_ARG, "null argument");
+    *dptr = dom->d_peer_flags;
+    return STKB_OK;
+}
+
+int stkb_buffer_ptr(stkb_domain* dom, int32_t buffer, void** dptr) {
+    if (!dom || !dptr) return fail(STKB_ERR_ARG, "null argument");
+    if (buffer < 0 || buffer >= dom->desc.n_grids) return fail(STKB_ERR_ARG, "buffer index out of range");
+    *dptr = dom->bufs[buffer];
+    return STKB_OK;
+}
+
+int stkb_ipc_open(int32_t device, const void* handle, void** dptr) {
+    if (!handle || !dptr) return fail(STKB_ERR_ARG, "null argument");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return STKB_OK;
+}
+
+int stkb_ipc_close(int32_t device, void* dptr) {
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+    return STKB_OK;
+}
+
+int stkb_set_peer(stkb_domain* dom, int32_t side, int32_t n_bufs, void* const* bufs, void* flags, int64_t peer_n0) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (side < 0 || side > 1) return fail(STKB_ERR_ARG, "side is 0 (lower) or 1 (upper)");
+    auto& p = dom->peer[side];
+    if (!bufs) {  // detach
+        p = stkb_domain::Peer();
+        return STKB_OK;
+    }
+    if (n_bufs != dom->desc.n_grids || !flags) return fail(STKB_ERR_ARG, "peer needs one pointer per buffer and its flags");
+    p.bufs.assign(bufs, bufs + n_bufs);
+    p.flags = static_cast<int32_t*>(flags);
+    p.n0 = peer_n0;
+    p.set = true;
+    return STKB_OK;
+}
+
+static PFN_cuStreamWaitValue32_v2 get_wait_fn() {
+    static PFN_cuStreamWaitValue32_v2 fn_ = nullptr;
+    if (!fn_) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+            fn_ = reinterpret_cast<PFN_cuStreamWaitValue32_v2>(fn);
+    }
+    return fn_;
+}
+
+int stkb_peer_signal(stkb_domain* dom, void* stream, int32_t value) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    static PFN_cuStreamWriteValue32_v2 write_fn = nullptr;
+    if (!write_fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(STKB_ERR_CUDA, "cuStreamWriteValue32 entry point unavailable");
+        write_fn = reinterpret_cast<PFN_cuStreamWriteValue32_v2>(fn);
+    }
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    CUstream st = static_cast<CUstream>(stream ? stream : dom->stream);
+    for (int side = 0; side < 2; ++side) {
+        const auto& p = dom->peer[side];
+        if (!p.set) continue;
+        // I am my lower neighbour's upper neighbour (its slot 1) and vice versa;
+        // the default flags fence this write after every prior store of the stream
+        int32_t* slot = p.flags + (side == 0 ? 1 : 0);
+        CUresult r = write_fn(st, reinterpret_cast<CUdeviceptr>(slot), cuuint32_t(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(int(r)));
+    }
+    return STKB_OK;
+}
+
+int stkb_peer_wait(stkb_domain* dom, void* stream, int32_t value) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    PFN_cuStreamWaitValue32_v2 wait_fn = get_wait_fn();
+    if (!wait_fn) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 entry point unavailable");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    CUstream st = static_cast<CUstream>(stream ? stream : dom->stream);
+    for (int side = 0; side < 2; ++side) {
+        if (!dom->peer[side].set) continue;
+        CUresult r = wait_fn(st, reinterpret_cast<CUdeviceptr>(dom->d_peer_flags + side), cuuint32_t(value),
+                             CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(int(r)));
+    }
+    return STKB_OK;
+}
+
 int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, int32_t value) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
-    static PFN_cuStreamWaitValue32_v2 wait_fn = nullptr;
-    if (!wait_fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-            return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 entry point unavailable");
-        wait_fn = reinterpret_cast<PFN_cuStreamWaitValue32_v2>(fn);
-    }
+    PFN_cuStreamWaitValue32_v2 wait_fn = get_wait_fn();
+    if (!wait_fn) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 entry point unavailable");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     int32_t* sig = dom->d_flags + kMaxTags + kMaxMaps + dom->maps[map_index].slot;
     CUresult r = wait_fn(static_cast<CUstream>(stream ? stream : dom->stream), reinterpret_cast<CUdeviceptr>(sig),

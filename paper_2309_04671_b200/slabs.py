@@ -215,10 +215,47 @@ def boundary_ranges(n: int, r: int) -> list:
     return out
 
 
-class DeviceSlabEngine:
-    """The rank-local slab on this GPU: a DeviceTarget driven map by map."""
+def run_step_p2p(eng) -> None:
+    """One time step with the fused halo push (stkb_launch_map_push).
 
-    def __init__(self, body: tuple, decls: dict, plan: SlabPlan, device: int, precision: str = "fast"):
+    Every exchanged map is ONE launch whose boundary output planes are also
+    stored into the z-neighbours' halos over NVLink.  The ranks count their
+    exchanged launches; before launch c a rank's stream waits until both
+    neighbours have finished launch c-1 (so the halo planes launch c reads
+    have landed, and the halo planes it pushes into are no longer read), and
+    after it writes c into both neighbours' flags.  Only stream memory
+    operations order the ranks; no kernel ever waits on another."""
+    from . import _lib as L
+
+    if eng.plan.world > 1 and not eng.peers_connected:
+        raise RuntimeError("p2p transport: connect the slab neighbours first (connect_ipc / connect_local)")
+    stream = ctypes.c_void_p(eng.compute.cuda_stream)
+    for i, s in enumerate(eng.body):
+        if stmt_kind(s) == "BoundSwap":
+            eng.swap(s.first, s.second)
+            continue
+        ex = eng.sched[i]
+        if ex and eng.plan.world > 1:
+            eng.t += 1
+            if eng.t > 1:
+                L.call("stkb_peer_wait", eng.dt.h, stream, ctypes.c_int32(eng.t - 1))
+            L.call("stkb_launch_map_push", eng.dt.h, eng.map_index[i], max(ex.values()))
+            eng.launches += 1
+            L.call("stkb_peer_signal", eng.dt.h, stream, ctypes.c_int32(eng.t))
+        else:
+            eng.launch(i, 0, eng.plan.size)
+
+
+class DeviceSlabEngine:
+    """The rank-local slab on this GPU: a DeviceTarget driven map by map.
+
+    transport "p2p" (default for streaming maps): the halo exchange is fused
+    into the compute kernel as peer-memory stores (connect with
+    :meth:`connect_ipc` across processes or :func:`connect_local` in one
+    process); "nccl": boundary items first, NCCL send/recv on a side stream."""
+
+    def __init__(self, body: tuple, decls: dict, plan: SlabPlan, device: int, precision: str = "fast",
+                 transport: Optional[str] = None):
         import torch
 
         from .backend import DeviceTarget
@@ -248,7 +285,17 @@ class DeviceSlabEngine:
         self.tdtype = torch.float32 if d0.dtype == "f32" else torch.float64
         self.launches = 0
         self.signal_target = {}  # map index -> running sum of its boundary signal
-        if plan.world > 1:
+        self.t = 0  # exchanged launches issued (p2p flags)
+        self._dist = None
+        self.peers_connected = False
+        streaming = all(p.kind in ("star", "wave", "box") for p in self.dt.plans) and len(decls_shape(decls)) == 3
+        import os as _os
+
+        self.transport = transport or _os.environ.get("STKB_TRANSPORT") or ("p2p" if streaming else "nccl")
+        if self.transport == "p2p" and not streaming:
+            raise ValueError("the fused p2p halo push needs 3-D streaming maps; use transport='nccl'")
+        self._ipc_opened = []
+        if plan.world > 1 and self.transport == "nccl":
             import os
 
             from . import _lib as L
@@ -315,10 +362,95 @@ class DeviceSlabEngine:
         self.compute.wait_stream(self.comm)
 
     def step(self, dist, group=None) -> None:
-        run_step(self, dist, group)
+        if self.transport == "p2p":
+            run_step_p2p(self)
+        else:
+            run_step(self, dist, group)
+
+    def finish(self) -> None:
+        """p2p: order the compute stream after the neighbours' last pushes into this slab's halos."""
+        from . import _lib as L
+
+        if self.transport == "p2p" and self.plan.world > 1 and self.t > 0:
+            L.call("stkb_peer_wait", self.dt.h, ctypes.c_void_p(self.compute.cuda_stream), ctypes.c_int32(self.t))
+
+    def _handles(self) -> dict:
+        from . import _lib as L
+
+        bufs = []
+        for b in range(len(self.dt.names)):
+            h = ctypes.create_string_buffer(64)
+            L.call("stkb_buffer_ipc_handle", self.dt.h, b, h)
+            bufs.append(h.raw)
+        f = ctypes.create_string_buffer(64)
+        L.call("stkb_flags_ipc_handle", self.dt.h, f)
+        return {"bufs": bufs, "flags": f.raw, "n0": self.plan.size}
+
+    def connect_ipc(self, dist) -> None:
+        """Exchange CUDA IPC handles with the z-neighbours and map their buffers."""
+        from . import _lib as L
+
+        self._dist = dist
+        mine = self._handles()
+        every = [None] * self.plan.world
+        dist.all_gather_object(every, mine)
+        for side, peer in ((0, self.plan.lower), (1, self.plan.upper)):
+            if peer is None:
+                continue
+            info = every[peer]
+            ptrs = []
+            for raw in info["bufs"] + [info["flags"]]:
+                p = ctypes.c_void_p()
+                L.call("stkb_ipc_open", self.dt.device, ctypes.create_string_buffer(raw, 64), ctypes.byref(p))
+                ptrs.append(p.value)
+                self._ipc_opened.append(p.value)
+            arr = (ctypes.c_void_p * (len(ptrs) - 1))(*ptrs[:-1])
+            L.call("stkb_set_peer", self.dt.h, side, len(ptrs) - 1, arr, ctypes.c_void_p(ptrs[-1]),
+                   ctypes.c_int64(info["n0"]))
+        self.peers_connected = True
 
     def close(self):
+        from . import _lib as L
+
+        if getattr(self, "dt", None) is None:
+            return
+        self.torch.cuda.synchronize(self.dt.device)
+        for p in self._ipc_opened:
+            L.call("stkb_ipc_close", self.dt.device, ctypes.c_void_p(p))
+        self._ipc_opened = []
+        if self._dist is not None:
+            self._dist.barrier()  # no neighbour still maps (or writes) these buffers
+            self._dist = None
         self.dt.close()
+        self.dt = None
+
+
+def connect_local(engines: list) -> None:
+    """Wire in-process slab engines (same GPU or peer-accessible GPUs) as z-neighbours."""
+    from . import _lib as L
+
+    def ptrs(e):
+        out = []
+        for b in range(len(e.dt.names)):
+            p = ctypes.c_void_p()
+            L.call("stkb_buffer_ptr", e.dt.h, b, ctypes.byref(p))
+            out.append(p.value)
+        f = ctypes.c_void_p()
+        L.call("stkb_flags_ptr", e.dt.h, ctypes.byref(f))
+        return out, f.value
+
+    for i, e in enumerate(engines):
+        for side, j in ((0, i - 1), (1, i + 1)):
+            if 0 <= j < len(engines):
+                bufs, flags = ptrs(engines[j])
+                arr = (ctypes.c_void_p * len(bufs))(*bufs)
+                L.call("stkb_set_peer", e.dt.h, side, len(bufs), arr, ctypes.c_void_p(flags),
+                       ctypes.c_int64(engines[j].plan.size))
+        e.peers_connected = True
+
+
+def decls_shape(decls: dict) -> tuple:
+    return tuple(next(iter(decls.values())).shape)
 
 
 def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Optional[int] = None,
@@ -342,6 +474,8 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
     names = list(local_grids)
     glob = {n: _Decl(g, slab) for n, g in local_grids.items()}
     eng = DeviceSlabEngine(tuple(loop.body), glob, slab, default_device() if device is None else device, precision)
+    if eng.transport == "p2p" and slab.world > 1:
+        eng.connect_ipc(dist)
     dead = dead_on_entry(bound.stmts, names, bindings or {})
     try:
         for n in names:
@@ -351,6 +485,7 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
         eng.dt.sync()
         for _ in range(count):
             eng.step(dist)
+        eng.finish()
         eng.torch.cuda.synchronize()
         out = {}
         for n in names:
@@ -433,6 +568,8 @@ class SlabBench:
         order = next(iter(decls.values())).order
         self.plan = SlabPlan(shape[0], world, rank, order)
         self.eng = DeviceSlabEngine(body, decls, self.plan, device)
+        if self.eng.transport == "p2p" and world > 1:
+            self.eng.connect_ipc(dist)
         self.local_points = self.plan.size * int(np.prod(shape[1:]))
         self.kind = self.eng.dt.plans[0].kind
         self._fill(builder, decls)
@@ -448,6 +585,7 @@ class SlabBench:
     def warmup(self, w: int) -> None:
         for _ in range(w):
             self.eng.step(self.dist)
+        self.eng.finish()
         self.torch.cuda.synchronize()
         self.dist.barrier()
 
@@ -460,6 +598,7 @@ class SlabBench:
         s.record(self.eng.compute)
         for _ in range(k):
             self.eng.step(self.dist)
+        self.eng.finish()
         e.record(self.eng.compute)
         torch.cuda.synchronize()
         self.dist.barrier()
@@ -470,7 +609,10 @@ class SlabBench:
         lay = self.eng.dt.layout()
         esz = 4 if self.eng.tdtype == self.torch.float32 else 8
         r = max((max(x.values()) for x in ex), default=0)
-        return {"backend": "nccl send/recv (batch_isend_irecv) on a side stream, overlapped with the interior",
+        backend = ("fused: boundary planes stored into the neighbours' halos over NVLink by the compute kernel "
+                   "(CUDA IPC peer pointers), stream-memop step flags") if self.eng.transport == "p2p" else \
+            "nccl send/recv (batch_isend_irecv) on a side stream, overlapped with the interior"
+        return {"backend": backend, "transport": self.eng.transport,
                 "planes_per_message": r, "bytes_per_message": r * lay["plane"] * esz,
                 "slab_planes": self.plan.size}
 

@@ -1,11 +1,15 @@
-"""Device z-slab engine on one B200 (the NCCL transport replaced by a mailbox).
+"""Device z-slab engine on one B200.
 
-Two (or three) DeviceSlabEngines — the real per-rank GPU objects, with their
+Two to four DeviceSlabEngines — the real per-rank GPU objects, with their
 compute/comm streams, boundary-first launches, plane spans and swaps — run
-on one GPU; a fake ``dist`` pairs each rank's sends with the peer's receives
-and performs them as device copies once every rank has posted the step.  No
-kernel ever waits on another rank's kernel.  Results are checked against
-the unsplit CPU oracle (bitwise for precision="exact").
+on one GPU.  transport "nccl": a fake ``dist`` pairs each rank's sends with
+the peer's receives and performs them as device copies once every rank has
+posted the step.  transport "p2p": the engines are wired with
+``connect_local`` and the compute kernels push their boundary planes straight
+into the neighbours' halos, ordered by stream memory operations; a second
+test runs two real processes that exchange CUDA IPC handles.  No kernel ever
+waits on another rank's kernel.  Results are checked against the unsplit CPU
+oracle (bitwise for precision="exact").
 """
 
 from __future__ import annotations
@@ -70,14 +74,23 @@ def _case(builder, shape, steps, dtype="f32"):
     return bound, decls, grids
 
 
-@pytest.mark.parametrize("world,builder,shape,steps,precision", [
+CASES = [
     (2, "star3d4r_norm", (40, 36, 140), 6, "fast"),
     (3, "star3d4r", (37, 20, 64), 4, "exact"),
     (2, "wave", (32, 24, 72), 8, "fast"),
     (2, "wave", (24, 16, 40), 4, "exact"),
     (4, "jacobi7", (48, 30, 70), 10, "fast"),
-])
-def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precision):
+    (3, "star3d4r", (27, 33, 100), 7, "fast"),   # slabs of 9 planes: pushes from both sides meet
+    (4, "star3d2r", (30, 20, 50), 5, "fast"),
+    (2, "wave", (20, 18, 36), 9, "fast"),
+]
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("world,builder,shape,steps,precision", CASES)
+def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precision, transport):
+    if transport == "p2p" and precision == "exact":
+        pytest.skip("the fused push serves the streaming (fast) maps; exact runs over NCCL")
     bound, decls, grids = _case(builder, shape, steps)
     body = bound.stmts[0].body
     order = next(iter(decls.values())).order
@@ -85,15 +98,25 @@ def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precisi
     engines = []
     for r in range(world):
         plan = SlabPlan(shape[0], world, r, order)
-        eng = DeviceSlabEngine(body, decls, plan, device=0, precision=precision)
+        eng = DeviceSlabEngine(body, decls, plan, device=0, precision=precision, transport=transport)
         for n in decls:
             eng.dt.upload(n, np.ascontiguousarray(grids[n].data[plan.global_slice()]))
         engines.append(eng)
+    if transport == "p2p":
+        from paper_2309_04671_b200.slabs import connect_local
+
+        connect_local(engines)
     for _ in range(steps):
         for r, eng in enumerate(engines):
             fake.rank = r
             eng.step(fake)
-        fake.resolve()
+        if transport == "nccl":
+            fake.resolve()
+    for eng in engines:
+        eng.finish()
+    import torch
+
+    torch.cuda.synchronize()
     ref = oracle.run_target_c(bound, grids)
     for n in decls:
         parts = []
@@ -107,6 +130,17 @@ def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precisi
             assert np.array_equal(got.data, ref[n].data), n
         else:
             assert compare(ref[n], got).max_relative <= 1e-5, (n, compare(ref[n], got).render())
+    # the exchanged d0 halo planes hold the neighbour's boundary planes bit for bit
+    reach = max((max(x.values()) for x in engines[0].sched if x), default=0)
+    for n in decls:
+        full = [eng.dt.download(n) for eng in engines]
+        o = engines[0].dt.order
+        for r in range(world - 1):
+            size = engines[r].plan.size
+            up = full[r][o + size:o + size + reach, o:-o, o:-o]
+            assert np.array_equal(up, full[r + 1][o:o + reach, o:-o, o:-o]), (n, r, "upper halo")
+            lo = full[r + 1][o - reach:o, o:-o, o:-o]
+            assert np.array_equal(lo, full[r][o + size - reach:o + size, o:-o, o:-o]), (n, r, "lower halo")
     for eng in engines:
         eng.close()
 
@@ -125,3 +159,35 @@ def test_run_slab_single_rank_matches_run_gpu():
     ref = run_gpu(bound, plan, grids, device=0)
     for n in grids:
         assert np.array_equal(got[n].data, ref[n].data), n
+
+
+@pytest.mark.parametrize("builder,shape,steps", [
+    ("star3d4r", (34, 28, 96), 5),
+    ("wave", (30, 20, 64), 6),
+])
+def test_two_process_ipc_push_matches_unsplit_oracle(tmp_path, builder, shape, steps):
+    """Two real processes exchange CUDA IPC handles (connect_ipc) and run run_slab with the fused push."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(here, "slab_ipc_worker.py"),
+           builder, ",".join(map(str, shape)), str(steps), str(tmp_path)]
+    env = dict(os.environ, STKB_TRANSPORT="p2p")
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    bound, decls, grids = _case(builder, shape, steps)
+    ref = oracle.run_target_c(bound, grids)
+    parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
+    for n in decls:
+        o = ref[n].order
+        got = GridBuffer(ref[n].dtype, ref[n].shape, o, np.zeros_like(ref[n].data))
+        got.interior[...] = np.concatenate([p[n][o:-o, o:-o, o:-o] for p in parts], axis=0)
+        rep = compare(ref[n], got)
+        assert rep.max_relative <= 1e-5, (n, rep.render())

@@ -165,20 +165,23 @@ int stkb_stream_wait_signal(stkb_domain *dom, void *stream, int32_t map_index, i
 int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (leave SMs for NCCL) */
 
 /* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process
- * per GPU).  Each rank exports its buffers and its 2-slot step-flag array with
- * CUDA IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and
+ * per GPU).  Each rank exports its buffers and its 2-slot flag array with CUDA
+ * IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and
  * registers them with stkb_set_peer (side 0 = lower neighbour, rank-1; side 1 =
  * upper, rank+1; buffer i of the neighbour pairs with my buffer i).
- * stkb_launch_map_push runs a map over its whole box and ALSO stores its first
- * / last `push_planes` output planes into the neighbours' halo planes from the
- * same kernel (peer-mapped st.global).  Ranks count their pushing launches;
- * launch c is bracketed by stkb_peer_wait(c-1) (both neighbours finished
- * launch c-1: their pushes into my halo are visible and they no longer read
- * the halo I will overwrite) and stkb_peer_signal(c) (a fenced stream write
- * into each neighbour's flag) — stream memory operations only: no kernel
- * ever waits on another.  This replaces the NCCL send/recv of the halo
- * planes (slabs.py run_step) for 3-D streaming maps. */
-int stkb_launch_map_push(stkb_domain *dom, int32_t map_index, int32_t push_planes);
+ * stkb_launch_map_pull runs a streaming map over its whole box; its TMA
+ * producer reads the src planes beyond the slab (q < 0, q >= n0) straight from
+ * the neighbours' buffers over NVLink instead of from this slab's halo — the
+ * halo exchange IS the kernel's own loads, no copy and no extra kernel.  Ranks
+ * count their pulling launches; launch c is bracketed by stkb_peer_wait(c-1)
+ * (both neighbours finished launch c-1: the planes I read are final) and
+ * stkb_peer_signal(c) (a fenced stream write into each neighbour's flag, so a
+ * neighbour's launch c+1 cannot overwrite planes my launch c still reads) —
+ * stream memory operations only: no kernel ever waits on another.
+ * stkb_peer_fetch_halo copies the neighbours' boundary planes into this
+ * slab's halo planes (after the last step, to return consistent slabs). */
+int stkb_launch_map_pull(stkb_domain *dom, int32_t map_index);
+int stkb_peer_fetch_halo(stkb_domain *dom, void *stream, int32_t planes);
 int stkb_buffer_ipc_handle(stkb_domain *dom, int32_t buffer, void *handle64);
 int stkb_flags_ipc_handle(stkb_domain *dom, void *handle64);
 int stkb_buffer_ptr(stkb_domain *dom, int32_t buffer, void **dptr);

@@ -33,7 +33,7 @@ EXPORTS = (
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
-    "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_push", "stkb_buffer_ipc_handle",
+    "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
     "stkb_flags_ipc_handle", "stkb_buffer_ptr", "stkb_flags_ptr", "stkb_ipc_open", "stkb_ipc_close", "stkb_set_peer",
     "stkb_peer_signal", "stkb_peer_wait",
 )
@@ -130,7 +130,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_launch_map_ranges": [V, i32, i32, P(i64), P(i64), i32, P(i32)],
         "stkb_stream_wait_signal": [V, V, i32, i32],
         "stkb_set_max_ctas": [V, i32],
-        "stkb_launch_map_push": [V, i32, i32],
+        "stkb_launch_map_pull": [V, i32],
+        "stkb_peer_fetch_halo": [V, V, i32],
         "stkb_buffer_ipc_handle": [V, i32, V],
         "stkb_flags_ipc_handle": [V, V],
         "stkb_buffer_ptr": [V, i32, P(V)],

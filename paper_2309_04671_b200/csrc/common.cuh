@@ -56,13 +56,12 @@ struct StarArgs {
     T cb[125];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 2
     int32_t store_hint;        // 1: streaming (evict-first) output stores
     int32_t order_y_fast;      // work items walk y tiles fastest
-    // fused halo push (multi-GPU z-slabs): output planes z < push_planes are also
-    // stored into the lower neighbour's top halo (its plane push_lo_n0 + z), planes
-    // z >= n0 - push_planes into the upper neighbour's bottom halo (plane z - n0)
-    T* push_lo;
-    T* push_hi;
-    int64_t push_lo_n0;
-    int32_t push_planes;
+    // fused halo exchange (multi-GPU z-slabs): src planes q < 0 are read by TMA
+    // straight from the lower neighbour's buffer (its plane pull_lo_n0 + q) when
+    // bit 0 of `pull` is set, planes q >= n0 from the upper neighbour's (plane q - n0)
+    // when bit 1 is — over NVLink, in place of this slab's own halo planes
+    int32_t pull;
+    int32_t pull_lo_n0;
 };
 
 // ---------------------------------------------------------------------------

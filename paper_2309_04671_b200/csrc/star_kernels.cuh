@@ -151,12 +151,14 @@ __device__ __noinline__ void store_row_masked(T* dz, T v0, T v1, T v2, T v3, int
         if (x + i >= lo2 && x + i < hi2) dz[i] = v[i];
 }
 
-template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL>
 __global__ void __launch_bounds__((NWY + 1) * 32, 1)
 star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_ctr,
                    const __grid_constant__ CUtensorMap tm_prev,
                    const __grid_constant__ CUtensorMap tm_vel,
+                   const __grid_constant__ CUtensorMap tm_lo,   // lower neighbour's src (a.pull & 1)
+                   const __grid_constant__ CUtensorMap tm_hi,   // upper neighbour's src (a.pull & 2)
                    const __grid_constant__ StarArgs<T> a) {
     using C = StarCfg<T, R, FORM, TY, NWY>;
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW;
@@ -188,6 +190,10 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             prefetch_tmap(&tm_src);
+            if constexpr (PULL) {
+                if (a.pull & 1) prefetch_tmap(&tm_lo);
+                if (a.pull & 2) prefetch_tmap(&tm_hi);
+            }
             if constexpr (FORM == FORM_WAVE) {
                 prefetch_tmap(&tm_ctr);
                 prefetch_tmap(&tm_prev);
@@ -220,11 +226,23 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     mbar_wait(&empty[s], ph ^ 1u);
                     stage_item[s] = item;
                     T* st = tiles + size_t(s) * C::STAGE_ELEMS;
+                    // src plane q: this slab's own (incl. its halo), or a neighbour's over NVLink
+                    const CUtensorMap* hm = &tm_src;
+                    int hz = q + int(a.g.order0);
+                    if constexpr (PULL) {
+                        if (q < 0 && (a.pull & 1)) {
+                            hm = &tm_lo;
+                            hz = q + a.pull_lo_n0 + int(a.g.order0);
+                        } else if (q >= int(a.g.n0) && (a.pull & 2)) {
+                            hm = &tm_hi;
+                            hz = q - int(a.g.n0) + int(a.g.order0);
+                        }
+                    }
                     if constexpr (FORM == FORM_WAVE) {
                         const int z = q - R;  // output plane completed at this step
                         const bool out = (z >= z0);
                         mbar_arrive_expect_tx(&full[s], C::HALO_BYTES + (out ? 3 * C::CTR_BYTES : 0));
-                        tma_load_3d(st, &tm_src, &full[s], c0, c1, q + int(a.g.order0));
+                        tma_load_3d(st, hm, &full[s], c0, c1, hz);
                         if (out) {
                             const int cx = int(a.g.lead) + x0;
                             const int cy = y0 + int(a.g.order);
@@ -235,7 +253,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                         }
                     } else {
                         mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
-                        tma_load_3d(st, &tm_src, &full[s], c0, c1, q + int(a.g.order0));
+                        tma_load_3d(st, hm, &full[s], c0, c1, hz);
                     }
                 }
             }
@@ -483,32 +501,6 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                                         outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2, a.box.hi2);
                             }
                         }
-                        if (a.push_planes > 0) {
-                            // fused halo exchange: the boundary planes go straight into the
-                            // neighbours' halo planes over NVLink (peer-mapped stores)
-#pragma unroll
-                            for (int side = 0; side < 2; ++side) {
-                                T* pbase = side == 0 ? a.push_lo : a.push_hi;
-                                const bool hit = side == 0 ? (z < a.push_planes) : (z >= a.g.n0 - a.push_planes);
-                                if (pbase != nullptr && hit) {
-                                    const int64_t zp = side == 0 ? z + a.push_lo_n0 : int64_t(z) - a.g.n0;
-                                    T* const pz = pbase + (dst0 - a.dst) + (zp + a.g.order0) * plane;
-                                    if (full_tile) {
-#pragma unroll
-                                        for (int j = 0; j < TY; ++j) stg16(pz + j * pitch, outv[j]);
-                                    } else if (x_any) {
-#pragma unroll
-                                        for (int j = 0; j < TY; ++j) {
-                                            const int y = y0 + jr0 + j;
-                                            if (y >= a.box.lo1 && y < a.box.hi1)
-                                                store_row_masked<T>(pz + j * pitch, outv[j][0], outv[j][1 % VEC],
-                                                                    outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2,
-                                                                    a.box.hi2);
-                                        }
-                                    }
-                                }
-                            }
-                        }
                     }
                 }
             }
@@ -577,10 +569,10 @@ inline int chunk_range(int lo, int n0, int lz, int tiles, int ctas, bool taper, 
     return k;
 }
 
-template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR>
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL>
 cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps, cudaStream_t stream) {
     using C = StarCfg<T, R, FORM, TY, NWY>;
-    auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR>;
+    auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR, PULL>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -636,7 +628,7 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     const int grid = a.n_items < ctas ? a.n_items : ctas;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], a);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], a);
     return cudaGetLastError();
 }
 
@@ -663,20 +655,32 @@ inline int star_variant_env() {
     return v;
 }
 
-template <typename T, int R, int V>
-cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
+template <typename T, int R, int V, bool PULL>
+cudaError_t launch_star_vp(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
     constexpr Variant vv = star_variant_of<T>(R, V);
     if (L.kind == 4) {
         if constexpr (R <= 2) {
-            if (L.has_divisor) return launch_star_cfg<T, R, FORM_BOX_DIV, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
-            return launch_star_cfg<T, R, FORM_BOX, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+            if (L.has_divisor)
+                return launch_star_cfg<T, R, FORM_BOX_DIV, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+            return launch_star_cfg<T, R, FORM_BOX, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
         } else {
             return cudaErrorInvalidValue;
         }
     }
-    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
-    if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
-    return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar>(L, a, maps, s);
+    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+    if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+    return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+}
+
+// the neighbour-reading (multi-GPU) kernels are separate instantiations: the
+// single-GPU launches run exactly the producer code they had without them
+template <typename T, int R, int V>
+cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
+    if (a.pull) {
+        if constexpr (V == 0) return launch_star_vp<T, R, V, true>(L, a, maps, s);
+        else return cudaErrorInvalidValue;  // built for the default variant only
+    }
+    return launch_star_vp<T, R, V, false>(L, a, maps, s);
 }
 
 #ifndef STKB_VARIANTS

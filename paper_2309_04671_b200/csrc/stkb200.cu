@@ -121,10 +121,11 @@ struct stkb_domain {
     int32_t* d_flags = nullptr;
     void* d_partials = nullptr;
     void* d_stage = nullptr;  // H2D staging: contiguous PCIe copies, then a repitch kernel
-    // z-slab neighbours for the fused halo push: [0] lower (rank-1), [1] upper (rank+1)
+    // z-slab neighbours for the fused halo exchange: [0] lower (rank-1), [1] upper (rank+1)
     struct Peer {
         bool set = false;
         std::vector<void*> bufs;  // the neighbour's buffer i (same binding history on every rank)
+        std::map<std::tuple<int, int, int>, CUtensorMap> tmaps;  // (buffer, box w, box h) over bufs
         int32_t* flags = nullptr; // the neighbour's step flags ([0] from its lower, [1] from its upper)
         int64_t n0 = 0;           // the neighbour's slab thickness
     } peer[2];
@@ -140,6 +141,25 @@ struct stkb_domain {
 
 namespace {
 
+// a 3-D tiled tensor map over one pitched grid buffer of `n0` interior planes
+int encode_tmap(stkb_domain* dom, void* base, int64_t n0, int bw, int bh, CUtensorMap* m) {
+    int rc = get_encoder();
+    if (rc) return rc;
+    const Geometry& g = dom->g;
+    cuuint64_t dims[3] = {cuuint64_t(g.pitch), cuuint64_t(g.n1 + 2 * g.order), cuuint64_t(n0 + 2 * g.order0)};
+    cuuint64_t strides[2] = {cuuint64_t(g.pitch * dom->elem), cuuint64_t(g.plane * dom->elem)};
+    cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(bh), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    CUresult r = g_encode(m, dom->elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                          3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promo[dom->l2promo & 3],
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return STKB_OK;
+}
+
 int encode_map(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap** out) {
     auto key = std::make_tuple(buffer, bw, bh);
     auto it = dom->tmaps.find(key);
@@ -147,22 +167,27 @@ int encode_map(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap**
         *out = &it->second;
         return STKB_OK;
     }
-    int rc = get_encoder();
-    if (rc) return rc;
     CUtensorMap m;
-    const Geometry& g = dom->g;
-    cuuint64_t dims[3] = {cuuint64_t(g.pitch), cuuint64_t(g.n1 + 2 * g.order), cuuint64_t(g.n0 + 2 * g.order0)};
-    cuuint64_t strides[2] = {cuuint64_t(g.pitch * dom->elem), cuuint64_t(g.plane * dom->elem)};
-    cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(bh), 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
-                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
-    CUresult r = g_encode(&m, dom->elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                          3, dom->bufs[buffer], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, promo[dom->l2promo & 3],
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    int rc = encode_tmap(dom, dom->bufs[buffer], dom->g.n0, bw, bh, &m);
+    if (rc) return rc;
     auto res = dom->tmaps.emplace(key, m);
+    *out = &res.first->second;
+    return STKB_OK;
+}
+
+// the same box over a z-neighbour's buffer (peer memory: TMA reads it over NVLink)
+int encode_peer_map(stkb_domain* dom, int side, int buffer, int bw, int bh, const CUtensorMap** out) {
+    auto& p = dom->peer[side];
+    auto key = std::make_tuple(buffer, bw, bh);
+    auto it = p.tmaps.find(key);
+    if (it != p.tmaps.end()) {
+        *out = &it->second;
+        return STKB_OK;
+    }
+    CUtensorMap m;
+    int rc = encode_tmap(dom, p.bufs[buffer], p.n0, bw, bh, &m);
+    if (rc) return rc;
+    auto res = p.tmaps.emplace(key, m);
     *out = &res.first->second;
     return STKB_OK;
 }
@@ -210,7 +235,7 @@ struct RangeSpec {
 
 template <typename T>
 int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind,
-                    const RangeSpec& rs = RangeSpec(), int push_planes = 0) {
+                    const RangeSpec& rs = RangeSpec(), bool pull = false) {
     const stkb_map_desc& d = op.d;
     if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
     StarArgs<T> a{};
@@ -237,13 +262,6 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.wave_b = T(d.wave_b);
     a.store_hint = dom->store_hint;
     a.order_y_fast = dom->order_y_fast;
-    if (push_planes > 0) {
-        const int db = bind[d.dst];
-        a.push_planes = push_planes;
-        a.push_lo = dom->peer[0].set ? static_cast<T*>(dom->peer[0].bufs[db]) : nullptr;
-        a.push_hi = dom->peer[1].set ? static_cast<T*>(dom->peer[1].bufs[db]) : nullptr;
-        a.push_lo_n0 = dom->peer[0].n0;
-    }
     if (d.kind == STKB_MAP_BOX)
         for (int i = 0; i < 125; ++i) a.cb[i] = T(d.box_coef[i]);
 
@@ -256,9 +274,19 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     int rc = encode_map(dom, sb, bx + 2 * hx, by + 2 * R, &m_halo);
 #endif
     if (rc) return rc;
-    CUtensorMap maps[4];
-    maps[0] = *m_halo;
-    maps[1] = maps[2] = maps[3] = *m_halo;
+    CUtensorMap maps[6];
+    for (int i = 0; i < 6; ++i) maps[i] = *m_halo;
+    if (pull) {
+        // src planes beyond this slab come straight from the neighbours' buffers
+        for (int side = 0; side < 2; ++side) {
+            if (!dom->peer[side].set) continue;
+            const CUtensorMap* pm;
+            if ((rc = encode_peer_map(dom, side, sb, bx + 2 * hx, by + 2 * R, &pm))) return rc;
+            maps[4 + side] = *pm;
+            a.pull |= 1 << side;
+        }
+        a.pull_lo_n0 = int32_t(dom->peer[0].n0);
+    }
     if (d.kind == STKB_MAP_WAVE) {
         const CUtensorMap *mc, *mp, *mv;
         if ((rc = encode_map(dom, sb, bx, by, &mc))) return rc;
@@ -847,17 +875,38 @@ int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges
     return rc;
 }
 
-int stkb_launch_map_push(stkb_domain* dom, int32_t map_index, int32_t push_planes) {
+int stkb_launch_map_pull(stkb_domain* dom, int32_t map_index) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     MapOp& op = dom->maps[map_index];
     if (op.d.kind == STKB_MAP_EXPR || dom->desc.ndim != 3)
-        return fail(STKB_ERR_UNSUPPORTED, "the fused halo push needs a 3-D streaming map");
-    if (push_planes < 0 || push_planes > dom->g.order0 || push_planes > dom->g.n0)
-        return fail(STKB_ERR_ARG, "push_planes must be in 0..min(order, n0)");
+        return fail(STKB_ERR_UNSUPPORTED, "the fused halo exchange needs a 3-D streaming map");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
-    return dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, RangeSpec(), push_planes)
-                                       : launch_star_map<double>(dom, op, dom->binding, RangeSpec(), push_planes);
+    return dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, RangeSpec(), true)
+                                       : launch_star_map<double>(dom, op, dom->binding, RangeSpec(), true);
+}
+
+int stkb_peer_fetch_halo(stkb_domain* dom, void* stream, int32_t planes) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (planes < 0 || planes > dom->g.order0) return fail(STKB_ERR_ARG, "planes must be in 0..order");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dom->stream;
+    const size_t pb = size_t(dom->g.plane) * dom->elem;
+    for (int side = 0; side < 2; ++side) {
+        const auto& p = dom->peer[side];
+        if (!p.set) continue;
+        const int64_t np = std::min<int64_t>(planes, p.n0);
+        if (np <= 0) continue;
+        // lower: my planes [order0 - np, order0) <- its [order0 + n0' - np, order0 + n0')
+        // upper: my planes [order0 + n0, order0 + n0 + np) <- its [order0, order0 + np)
+        const int64_t mine = side == 0 ? dom->g.order0 - np : dom->g.order0 + dom->g.n0;
+        const int64_t theirs = side == 0 ? dom->g.order0 + p.n0 - np : dom->g.order0;
+        for (int b = 0; b < dom->desc.n_grids; ++b)
+            CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dom->bufs[b]) + mine * pb,
+                                     static_cast<const char*>(p.bufs[b]) + theirs * pb, size_t(np) * pb,
+                                     cudaMemcpyDefault, s));
+    }
+    return STKB_OK;
 }
 
 int stkb_buffer_ipc_handle(stkb_domain* dom, int32_t buffer, void* handle) {
@@ -916,7 +965,9 @@ int stkb_set_peer(stkb_domain* dom, int32_t side, int32_t n_bufs, void* const* b
         return STKB_OK;
     }
     if (n_bufs != dom->desc.n_grids || !flags) return fail(STKB_ERR_ARG, "peer needs one pointer per buffer and its flags");
+    if (peer_n0 < dom->g.order0) return fail(STKB_ERR_ARG, "a neighbour slab must hold at least `order` planes");
     p.bufs.assign(bufs, bufs + n_bufs);
+    p.tmaps.clear();
     p.flags = static_cast<int32_t*>(flags);
     p.n0 = peer_n0;
     p.set = true;

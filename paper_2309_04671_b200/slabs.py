@@ -216,15 +216,16 @@ def boundary_ranges(n: int, r: int) -> list:
 
 
 def run_step_p2p(eng) -> None:
-    """One time step with the fused halo push (stkb_launch_map_push).
+    """One time step with the fused halo exchange (stkb_launch_map_pull).
 
-    Every exchanged map is ONE launch whose boundary output planes are also
-    stored into the z-neighbours' halos over NVLink.  The ranks count their
-    exchanged launches; before launch c a rank's stream waits until both
-    neighbours have finished launch c-1 (so the halo planes launch c reads
-    have landed, and the halo planes it pushes into are no longer read), and
-    after it writes c into both neighbours' flags.  Only stream memory
-    operations order the ranks; no kernel ever waits on another."""
+    Every streaming map is ONE launch whose TMA producer reads the src planes
+    beyond the slab straight from the z-neighbours' buffers over NVLink — no
+    halo copy, no exchange stream, no NCCL kernel.  The ranks count these
+    launches; before launch c a rank's stream waits until both neighbours have
+    finished launch c-1 (the planes it reads are final), and after it writes c
+    into both neighbours' flags (so a neighbour's launch c+1 cannot overwrite
+    planes launch c still reads).  Only stream memory operations order the
+    ranks; no kernel ever waits on another."""
     from . import _lib as L
 
     if eng.plan.world > 1 and not eng.peers_connected:
@@ -234,23 +235,22 @@ def run_step_p2p(eng) -> None:
         if stmt_kind(s) == "BoundSwap":
             eng.swap(s.first, s.second)
             continue
-        ex = eng.sched[i]
-        if ex and eng.plan.world > 1:
-            eng.t += 1
-            if eng.t > 1:
-                L.call("stkb_peer_wait", eng.dt.h, stream, ctypes.c_int32(eng.t - 1))
-            L.call("stkb_launch_map_push", eng.dt.h, eng.map_index[i], max(ex.values()))
-            eng.launches += 1
-            L.call("stkb_peer_signal", eng.dt.h, stream, ctypes.c_int32(eng.t))
-        else:
+        if eng.plan.world == 1:
             eng.launch(i, 0, eng.plan.size)
+            continue
+        eng.t += 1
+        if eng.t > 1:
+            L.call("stkb_peer_wait", eng.dt.h, stream, ctypes.c_int32(eng.t - 1))
+        L.call("stkb_launch_map_pull", eng.dt.h, eng.map_index[i])
+        eng.launches += 1
+        L.call("stkb_peer_signal", eng.dt.h, stream, ctypes.c_int32(eng.t))
 
 
 class DeviceSlabEngine:
     """The rank-local slab on this GPU: a DeviceTarget driven map by map.
 
     transport "p2p" (default for streaming maps): the halo exchange is fused
-    into the compute kernel as peer-memory stores (connect with
+    into the compute kernel as peer-memory TMA loads (connect with
     :meth:`connect_ipc` across processes or :func:`connect_local` in one
     process); "nccl": boundary items first, NCCL send/recv on a side stream."""
 
@@ -293,7 +293,7 @@ class DeviceSlabEngine:
 
         self.transport = transport or _os.environ.get("STKB_TRANSPORT") or ("p2p" if streaming else "nccl")
         if self.transport == "p2p" and not streaming:
-            raise ValueError("the fused p2p halo push needs 3-D streaming maps; use transport='nccl'")
+            raise ValueError("the fused p2p halo exchange needs 3-D streaming maps; use transport='nccl'")
         self._ipc_opened = []
         if plan.world > 1 and self.transport == "nccl":
             import os
@@ -367,12 +367,17 @@ class DeviceSlabEngine:
         else:
             run_step(self, dist, group)
 
-    def finish(self) -> None:
-        """p2p: order the compute stream after the neighbours' last pushes into this slab's halos."""
+    def finish(self, halo: bool = True) -> None:
+        """p2p: after the last step, wait for the neighbours' last launches and copy their
+        boundary planes into this slab's halo planes (the slabs returned then match the NCCL
+        transport's, halos included)."""
         from . import _lib as L
 
         if self.transport == "p2p" and self.plan.world > 1 and self.t > 0:
-            L.call("stkb_peer_wait", self.dt.h, ctypes.c_void_p(self.compute.cuda_stream), ctypes.c_int32(self.t))
+            stream = ctypes.c_void_p(self.compute.cuda_stream)
+            L.call("stkb_peer_wait", self.dt.h, stream, ctypes.c_int32(self.t))
+            if halo:
+                L.call("stkb_peer_fetch_halo", self.dt.h, stream, self.dt.order)
 
     def _handles(self) -> dict:
         from . import _lib as L
@@ -483,6 +488,8 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
                 continue  # fresh device grids are zero; this input is never observed
             eng.dt.upload(n, local_grids[n].data, sync=False)
         eng.dt.sync()
+        if eng.transport == "p2p" and slab.world > 1:
+            dist.barrier()  # every neighbour's slab is on its device before anyone reads it
         for _ in range(count):
             eng.step(dist)
         eng.finish()
@@ -574,6 +581,9 @@ class SlabBench:
         self.kind = self.eng.dt.plans[0].kind
         self._fill(builder, decls)
         self.torch = torch
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()  # every slab is filled before a neighbour reads it
 
     def _fill(self, builder, decls):
         import bench  # the synthetic device fill lives with the benchmark
@@ -585,7 +595,7 @@ class SlabBench:
     def warmup(self, w: int) -> None:
         for _ in range(w):
             self.eng.step(self.dist)
-        self.eng.finish()
+        self.eng.finish(halo=False)
         self.torch.cuda.synchronize()
         self.dist.barrier()
 
@@ -598,7 +608,7 @@ class SlabBench:
         s.record(self.eng.compute)
         for _ in range(k):
             self.eng.step(self.dist)
-        self.eng.finish()
+        self.eng.finish(halo=False)
         e.record(self.eng.compute)
         torch.cuda.synchronize()
         self.dist.barrier()
@@ -609,8 +619,8 @@ class SlabBench:
         lay = self.eng.dt.layout()
         esz = 4 if self.eng.tdtype == self.torch.float32 else 8
         r = max((max(x.values()) for x in ex), default=0)
-        backend = ("fused: boundary planes stored into the neighbours' halos over NVLink by the compute kernel "
-                   "(CUDA IPC peer pointers), stream-memop step flags") if self.eng.transport == "p2p" else \
+        backend = ("fused: the compute kernel's TMA reads the src planes beyond its slab straight from the "
+                   "neighbours' buffers over NVLink (CUDA IPC), stream-memop step flags") if self.eng.transport == "p2p" else \
             "nccl send/recv (batch_isend_irecv) on a side stream, overlapped with the interior"
         return {"backend": backend, "transport": self.eng.transport,
                 "planes_per_message": r, "bytes_per_message": r * lay["plane"] * esz,

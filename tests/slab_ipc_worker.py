@@ -1,8 +1,8 @@
-"""One rank of the two-process fused-halo-push test (test_gpu_slabs.py).
+"""One rank of the two-process fused-halo-exchange test (test_gpu_slabs.py).
 
 Launched by torch.distributed.run with the gloo backend (only for the IPC
-handle exchange and barriers: the halo planes travel inside the compute
-kernels over peer memory).  Both ranks use cuda:0 — CUDA IPC between two
+handle exchange and barriers: the halo planes are read by the compute
+kernels' TMA straight from the neighbour's buffers).  Both ranks use cuda:0 — CUDA IPC between two
 processes on one device — and each writes its final slab to <out>/rank<r>.npz.
 """
 

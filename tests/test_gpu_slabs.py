@@ -5,9 +5,10 @@ compute/comm streams, boundary-first launches, plane spans and swaps — run
 on one GPU.  transport "nccl": a fake ``dist`` pairs each rank's sends with
 the peer's receives and performs them as device copies once every rank has
 posted the step.  transport "p2p": the engines are wired with
-``connect_local`` and the compute kernels push their boundary planes straight
-into the neighbours' halos, ordered by stream memory operations; a second
-test runs two real processes that exchange CUDA IPC handles.  No kernel ever
+``connect_local`` and the compute kernels' TMA reads the src planes beyond
+their slab straight from the neighbours' buffers, ordered by stream memory
+operations; a second test runs two real processes that exchange CUDA IPC
+handles.  No kernel ever
 waits on another rank's kernel.  Results are checked against the unsplit CPU
 oracle (bitwise for precision="exact").
 """
@@ -80,7 +81,7 @@ CASES = [
     (2, "wave", (32, 24, 72), 8, "fast"),
     (2, "wave", (24, 16, 40), 4, "exact"),
     (4, "jacobi7", (48, 30, 70), 10, "fast"),
-    (3, "star3d4r", (27, 33, 100), 7, "fast"),   # slabs of 9 planes: pushes from both sides meet
+    (3, "star3d4r", (27, 33, 100), 7, "fast"),   # slabs of 9 planes: both neighbours read each slab
     (4, "star3d2r", (30, 20, 50), 5, "fast"),
     (2, "wave", (20, 18, 36), 9, "fast"),
 ]
@@ -90,7 +91,7 @@ CASES = [
 @pytest.mark.parametrize("world,builder,shape,steps,precision", CASES)
 def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precision, transport):
     if transport == "p2p" and precision == "exact":
-        pytest.skip("the fused push serves the streaming (fast) maps; exact runs over NCCL")
+        pytest.skip("the fused exchange serves the streaming (fast) maps; exact runs over NCCL")
     bound, decls, grids = _case(builder, shape, steps)
     body = bound.stmts[0].body
     order = next(iter(decls.values())).order
@@ -130,7 +131,7 @@ def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precisi
             assert np.array_equal(got.data, ref[n].data), n
         else:
             assert compare(ref[n], got).max_relative <= 1e-5, (n, compare(ref[n], got).render())
-    # the exchanged d0 halo planes hold the neighbour's boundary planes bit for bit
+    # the d0 halo planes hold the neighbour's boundary planes bit for bit (p2p: after finish())
     reach = max((max(x.values()) for x in engines[0].sched if x), default=0)
     for n in decls:
         full = [eng.dt.download(n) for eng in engines]
@@ -165,8 +166,8 @@ def test_run_slab_single_rank_matches_run_gpu():
     ("star3d4r", (34, 28, 96), 5),
     ("wave", (30, 20, 64), 6),
 ])
-def test_two_process_ipc_push_matches_unsplit_oracle(tmp_path, builder, shape, steps):
-    """Two real processes exchange CUDA IPC handles (connect_ipc) and run run_slab with the fused push."""
+def test_two_process_ipc_exchange_matches_unsplit_oracle(tmp_path, builder, shape, steps):
+    """Two real processes exchange CUDA IPC handles (connect_ipc) and run run_slab with the fused exchange."""
     import os
     import socket
     import subprocess

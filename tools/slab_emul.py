@@ -3,9 +3,9 @@
 Runs rank `r` of a `G`-way strong-scaling decomposition of a config with the
 real DeviceSlabEngine.  transport nccl: single launch, boundary items first,
 SM reservation, signal wait on the exchange stream, but a transport that
-moves no bytes.  transport p2p: the fused push with the rank wired to itself
-as both neighbours (the boundary planes land in its own halos, through HBM
-instead of NVLink; the step flags are its own).  Either way the measured step
+moves no bytes.  transport p2p: the fused exchange with the rank wired to
+itself as both neighbours (the TMA reads the planes beyond the slab from its
+own buffer, through HBM instead of NVLink; the step flags are its own).  Either way the measured step
 time is the compute-side critical path of one rank.
 
     python tools/slab_emul.py c4 8 [steps] [strong|weak] [nccl|p2p]

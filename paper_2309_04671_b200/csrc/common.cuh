@@ -175,7 +175,8 @@ struct StarLaunch {
     int kind;          // 1 = STAR, 2 = WAVE, 4 = BOX
     int radius;
     bool has_divisor;
-    const CUtensorMap* maps;  // [4]: src halo box, src centre box, prev centre box, vel centre box
+    const CUtensorMap* maps;  // [6]: src halo box, src/prev/vel centre boxes, lower/upper neighbour halo boxes
+    int box_w, box_h;  // halo box the tensor maps were encoded with (must equal the kernel's tile)
     int num_sms;
     int max_ctas;      // 0 = auto (one per SM)
     int lz;            // 0 = auto

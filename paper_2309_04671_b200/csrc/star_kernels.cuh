@@ -573,6 +573,9 @@ template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PU
 cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps, cudaStream_t stream) {
     using C = StarCfg<T, R, FORM, TY, NWY>;
     auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR, PULL>;
+    // a tensor-map box that differs from this instantiation's tile would make the
+    // mbarrier transaction counts disagree (a hang): refuse instead
+    if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -642,7 +645,18 @@ __host__ __device__ constexpr Variant star_variant_of(int R, int v) {
         case 1: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, true};   // wide rows, 1 warp pair / SMSP
         case 2: return Variant{R == 1 ? 6 : 3, 10, true};
         case 3: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, false};  // odd x-taps as re-paired FFMA2
-        default: return Variant{R == 1 ? 4 : 2, 15, true};                 // measured best on B200 (tools/sweep.py)
+        case 4: return Variant{1, 15, true};                                // one row per warp
+        case 5: return Variant{2, 11, true};                                // fewer warps, more registers
+        case 6: return Variant{2, 9, true};
+        case 7: return Variant{2, 12, true};
+        case 8: return Variant{3, 8, true};
+        default:  // measured best on B200 (tools/sweep.py)
+            if (sizeof(T) == 8) {
+                if (R == 1) return Variant{1, 15, true};
+                if (R == 2) return Variant{2, 9, true};
+                if (R == 4) return Variant{2, 11, true};
+            }
+            return Variant{R == 1 ? 4 : 2, 15, true};
     }
 }
 
@@ -694,6 +708,11 @@ cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUten
             case 1: return launch_star_v<T, R, 1>(L, a, maps, s);
             case 2: return launch_star_v<T, R, 2>(L, a, maps, s);
             case 3: return launch_star_v<T, R, 3>(L, a, maps, s);
+            case 4: return launch_star_v<T, R, 4>(L, a, maps, s);
+            case 5: return launch_star_v<T, R, 5>(L, a, maps, s);
+            case 6: return launch_star_v<T, R, 6>(L, a, maps, s);
+            case 7: return launch_star_v<T, R, 7>(L, a, maps, s);
+            case 8: return launch_star_v<T, R, 8>(L, a, maps, s);
             default: break;
         }
     }

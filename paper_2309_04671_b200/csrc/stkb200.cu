@@ -301,6 +301,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.radius = R;
     L.has_divisor = d.divisor != 0.0;
     L.maps = maps;
+    L.box_w = bx + 2 * hx;
+    L.box_h = by + 2 * R;  // (STKB_EXP_NOYHALO loads fewer rows; the stage keeps this shape)
     L.num_sms = dom->num_sms;
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;

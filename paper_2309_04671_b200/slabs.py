@@ -296,14 +296,30 @@ class DeviceSlabEngine:
             raise ValueError("the fused p2p halo exchange needs 3-D streaming maps; use transport='nccl'")
         self._ipc_opened = []
         if plan.world > 1 and self.transport == "nccl":
-            import os
+            self._reserve_nccl_sms()
 
-            from . import _lib as L
+    def _reserve_nccl_sms(self) -> None:
+        import os
 
-            # leave SMs free so NCCL's copy kernels run while the interior computes
-            sms = torch.cuda.get_device_properties(device).multi_processor_count
-            reserve = int(os.environ.get("STKB_NCCL_SMS", "4"))
-            L.call("stkb_set_max_ctas", self.dt.h, max(1, sms - reserve))
+        from . import _lib as L
+
+        # leave SMs free so NCCL's copy kernels run while the interior computes
+        sms = self.torch.cuda.get_device_properties(self.dt.device).multi_processor_count
+        reserve = int(os.environ.get("STKB_NCCL_SMS", "4"))
+        L.call("stkb_set_max_ctas", self.dt.h, max(1, sms - reserve))
+
+    def _device_uuid(self, ordinal: int) -> str:
+        return str(getattr(self.torch.cuda.get_device_properties(ordinal), "uuid", ordinal))
+
+    def _can_reach(self, uuid: str) -> bool:
+        """Can this GPU read memory on the GPU with this uuid (same device, or peer access)?"""
+        me = self.dt.device
+        if uuid == self._device_uuid(me):
+            return True
+        for d in range(self.torch.cuda.device_count()):
+            if self._device_uuid(d) == uuid:
+                return bool(self.torch.cuda.can_device_access_peer(me, d))
+        return False
 
     def view(self, name: str, z0: int, n: int):
         from . import _lib as L
@@ -392,13 +408,28 @@ class DeviceSlabEngine:
         return {"bufs": bufs, "flags": f.raw, "n0": self.plan.size}
 
     def connect_ipc(self, dist) -> None:
-        """Exchange CUDA IPC handles with the z-neighbours and map their buffers."""
+        """Exchange CUDA IPC handles with the z-neighbours and map their buffers.
+
+        If any rank cannot reach a neighbour's GPU (no peer access), every rank falls
+        back to the NCCL transport together (the decision is collective)."""
         from . import _lib as L
 
         self._dist = dist
         mine = self._handles()
+        mine["uuid"] = self._device_uuid(self.dt.device)
         every = [None] * self.plan.world
         dist.all_gather_object(every, mine)
+        ok = all(self._can_reach(every[p]["uuid"]) for p in (self.plan.lower, self.plan.upper) if p is not None)
+        votes = [None] * self.plan.world
+        dist.all_gather_object(votes, ok)
+        if not all(votes):
+            import warnings
+
+            warnings.warn("z-slab neighbours without peer access: halo exchange falls back to NCCL")
+            self.transport = "nccl"
+            self._reserve_nccl_sms()
+            self._dist = None
+            return
         for side, peer in ((0, self.plan.lower), (1, self.plan.upper)):
             if peer is None:
                 continue

@@ -32,10 +32,10 @@ cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cuda
 }
 
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x) {
-    (void)kind;
     if (radius < 1 || radius > 4) return 1;
-    if (dtype == 1) star_tile_t<float>(radius, bx, by, halo_x);
-    else star_tile_t<double>(radius, bx, by, halo_x);
+    const bool box = kind == 4;  // STKB_MAP_BOX
+    if (dtype == 1) star_tile_t<float>(radius, box, bx, by, halo_x);
+    else star_tile_t<double>(radius, box, bx, by, halo_x);
     return 0;
 }
 }  // namespace stkb

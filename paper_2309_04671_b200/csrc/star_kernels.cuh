@@ -639,7 +639,7 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
 struct Variant { int ty, nwy; bool odd_scalar; };
 
 template <typename T>
-__host__ __device__ constexpr Variant star_variant_of(int R, int v) {
+__host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = false) {
     if (sizeof(T) == 8 && v == 9) return Variant{R == 1 ? 8 : 4, 7, true};  // previous fp64 default
     switch (v) {
         case 1: return Variant{R == 1 ? 8 : (R == 2 ? 6 : 4), 7, true};   // wide rows, 1 warp pair / SMSP
@@ -650,13 +650,11 @@ __host__ __device__ constexpr Variant star_variant_of(int R, int v) {
         case 6: return Variant{2, 9, true};
         case 7: return Variant{2, 12, true};
         case 8: return Variant{3, 8, true};
-        default:  // measured best on B200 (tools/sweep.py)
-            if (sizeof(T) == 8) {
-                if (R == 1) return Variant{1, 15, true};
-                if (R == 2) return Variant{2, 9, true};
-                if (R == 4) return Variant{2, 11, true};
-            }
-            return Variant{R == 1 ? 4 : 2, 15, true};
+        default:  // measured best on B200 per form, dtype and radius (tools/sweep.py)
+            if (box) return Variant{R == 1 ? 4 : 1, 15, true};  // dense cube (R=2: 125 taps, one row per warp)
+            if (R == 1) return Variant{1, 15, true};
+            if (R == 2) return sizeof(T) == 8 ? Variant{2, 9, true} : Variant{1, 15, true};
+            return Variant{2, 11, true};
     }
 }
 
@@ -674,9 +672,10 @@ cudaError_t launch_star_vp(const StarLaunch& L, const StarArgs<T>& a, const CUte
     constexpr Variant vv = star_variant_of<T>(R, V);
     if (L.kind == 4) {
         if constexpr (R <= 2) {
+            constexpr Variant vb = star_variant_of<T>(R, V, true);
             if (L.has_divisor)
-                return launch_star_cfg<T, R, FORM_BOX_DIV, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
-            return launch_star_cfg<T, R, FORM_BOX, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+                return launch_star_cfg<T, R, FORM_BOX_DIV, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
+            return launch_star_cfg<T, R, FORM_BOX, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
         } else {
             return cudaErrorInvalidValue;
         }
@@ -732,10 +731,10 @@ cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUten
 
 // tile geometry used to build the tensor-map boxes on the host
 template <typename T>
-inline void star_tile_t(int R, int* bx, int* by, int* halo_x) {
+inline void star_tile_t(int R, bool box, int* bx, int* by, int* halo_x) {
     constexpr int VEC = 16 / sizeof(T);
     const int v = STKB_VARIANTS > 1 ? star_variant_env() : 0;
-    const Variant vv = star_variant_of<T>(R, v);
+    const Variant vv = star_variant_of<T>(R, v, box);
     *bx = 32 * VEC;
     *by = vv.nwy * vv.ty;
     *halo_x = ((R + VEC - 1) / VEC) * VEC;

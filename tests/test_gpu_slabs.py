@@ -65,8 +65,8 @@ class MailboxDist:
         torch.cuda.synchronize()
 
 
-def _case(builder, shape, steps, dtype="f32"):
-    bound, decls = corpus.config_target(builder, shape, steps, dtype)
+def _case(builder, shape, steps, dtype="f32", width=0, scheme="cross_product"):
+    bound, decls = corpus.config_target(builder, shape, steps, dtype, map_width=width, scheme=scheme)
     grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
     if builder == "wave":
         corpus.wave_inputs(grids)
@@ -84,15 +84,23 @@ CASES = [
     (3, "star3d4r", (27, 33, 100), 7, "fast"),   # slabs of 9 planes: both neighbours read each slab
     (4, "star3d2r", (30, 20, 50), 5, "fast"),
     (2, "wave", (20, 18, 36), 9, "fast"),
+    (3, "star3d4r_norm", (40, 36, 72), 5, "fast", "f32", 3, "cross_product"),  # PML regions, clipped per slab
+    (2, "star3d4r_norm", (32, 24, 40), 4, "fast", "f32", 5, "slab7"),
+    (2, "j3d27pt", (30, 26, 70), 6, "fast"),                                 # dense box form
+    (2, "star3d2r_norm", (28, 20, 36), 5, "fast", "f64"),
+    (3, "wave", (27, 16, 40), 5, "fast", "f64"),
 ]
 
 
 @pytest.mark.parametrize("transport", ["nccl", "p2p"])
-@pytest.mark.parametrize("world,builder,shape,steps,precision", CASES)
-def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precision, transport):
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c[:2] + c[4:])))
+def test_device_slabs_match_unsplit_oracle(case, transport):
+    world, builder, shape, steps, precision, *extra = case
+    dtype = extra[0] if extra else "f32"
+    width, scheme = (extra[1], extra[2]) if len(extra) > 1 else (0, "cross_product")
     if transport == "p2p" and precision == "exact":
         pytest.skip("the fused exchange serves the streaming (fast) maps; exact runs over NCCL")
-    bound, decls, grids = _case(builder, shape, steps)
+    bound, decls, grids = _case(builder, shape, steps, dtype, width, scheme)
     body = bound.stmts[0].body
     order = next(iter(decls.values())).order
     fake = MailboxDist()
@@ -130,7 +138,8 @@ def test_device_slabs_match_unsplit_oracle(world, builder, shape, steps, precisi
         if precision == "exact":
             assert np.array_equal(got.data, ref[n].data), n
         else:
-            assert compare(ref[n], got).max_relative <= 1e-5, (n, compare(ref[n], got).render())
+            tol = 1e-12 if dtype == "f64" else 1e-5
+            assert compare(ref[n], got).max_relative <= tol, (n, compare(ref[n], got).render())
     # the d0 halo planes hold the neighbour's boundary planes bit for bit (p2p: after finish())
     reach = max((max(x.values()) for x in engines[0].sched if x), default=0)
     for n in decls:

@@ -1,13 +1,15 @@
 // 1.5D d0-streaming star kernels for 2-D grids (the reference's 2-D streaming
 // plan, planning.py:78-86 `streaming_1_5d`: d0 is streamed, d1 is the lane axis).
 //
-// A 2-D grid of the paper's size (Listing 1: 1000^2, 4 MB fp32) lives in L2, so
-// the design drops the TMA/shared-memory staging of the 3-D kernel: each warp
-// owns 32 x VEC consecutive d1 points and a chunk of d0 rows; every lane
-// fetches its row segment plus the d1 halo with 128-bit loads (neighbouring
-// lanes share L1 lines), and the d0 taps go through the same (2R+1)-deep
-// register accumulator ring (static slots, loop unrolled by 2R+1) and packed
-// FFMA2 math as the 3-D kernel.
+// Each warp owns 32 x VEC consecutive d1 points and a chunk of d0 rows.  Rows
+// arrive through a per-warp shared-memory ring filled with asynchronous 16-byte
+// copies (cp.async.cg, L2 only): D rows are in flight per warp without holding
+// registers, which is what a bandwidth-bound 2-D sweep needs (a register
+// prefetch of one row per warp left HBM half idle).  The edge lanes also fetch
+// the d1 halo chunks, so every lane reads its row segment + halo from shared
+// memory with 128-bit loads; the d0 taps go through the same (2R+1)-deep
+// register accumulator ring (loop unrolled by 2R+1) and packed FFMA2 math as
+// the 3-D kernel.
 #include "star_kernels.cuh"
 
 namespace stkb {
@@ -30,22 +32,52 @@ struct Coef2D {
     T c0, cm0[4], cp0[4], cm1[4], cp1[4], rdiv;
 };
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    // src-size 0 zero-fills the 16 bytes without reading global memory
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+#ifndef STKB_2D_DEPTH
+#define STKB_2D_DEPTH 8
+#endif
+#ifndef STKB_2D_WARPS
+#define STKB_2D_WARPS 4
+#endif
+
+template <typename T, int R>
+struct Ring2D {
+    static constexpr int VEC = 16 / sizeof(T);
+    static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
+    static constexpr int NS = 2 * R + 1;
+    static constexpr int D = NS * ((STKB_2D_DEPTH + NS - 1) / NS);  // rows in flight per warp
+    static constexpr int SWR = 32 * VEC + 2 * RA;       // one ring row: left halo | 32 lanes | right halo
+    static constexpr int WARPS = STKB_2D_WARPS;
+    static constexpr size_t SMEM = size_t(WARPS) * D * SWR * sizeof(T);
+};
+
 template <typename T, int R, bool DIV>
-__global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __restrict__ src, T* __restrict__ dst,
                                                      const __grid_constant__ Star2DArgs a,
                                                      const __grid_constant__ Coef2D<T> cf) {
     using K = Pk<T>;
     using P = typename K::P;
-    constexpr int VEC = 16 / sizeof(T);
+    using G = Ring2D<T, R>;
+    constexpr int VEC = G::VEC, RA = G::RA, NS = G::NS, D = G::D, SWR = G::SWR;
     constexpr int W = K::W;
     constexpr int NPK = VEC / W;
-    constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
-    constexpr int NS = 2 * R + 1;
+    constexpr int NH = RA / VEC;  // 16-byte halo chunks per side
+    extern __shared__ __align__(16) unsigned char smem2d[];
     const int lane = threadIdx.x & 31;
+    T* const ring = reinterpret_cast<T*>(smem2d) + size_t(threadIdx.x >> 5) * D * SWR;
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= a.n_tx * a.n_tz) return;
+    if (wid >= a.n_tx * a.n_tz) return;  // whole warps only
     const int tx = wid % a.n_tx, tz = wid / a.n_tx;
-    const int x = a.x0base + (tx * 32 + lane) * VEC;
+    const int xw = a.x0base + tx * 32 * VEC;  // warp's first column
+    const int x = xw + lane * VEC;
     const int z0 = a.lo0 + tz * a.lz;
     const int z1 = min(z0 + a.lz, a.hi0);
     const int nq = (z1 - z0) + 2 * R;
@@ -57,33 +89,38 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
     const T* cmx = cf.cm1;
     const T* cpx = cf.cp1;
     const T rdiv = cf.rdiv;
-    const T* row0 = src + a.lead + x;  // + (q + order) * pitch
+    const T* wrow = src + a.lead + xw;  // + (q + order) * pitch
     T* out0 = dst + a.lead + x;
+    // column chunks past the padded row are zero-filled instead of read
+    const int64_t row_end = a.pitch - a.lead - xw;  // elements left in the row from xw
+    const bool c_ok = lane * VEC + VEC <= row_end;
+    const bool r_ok = lane >= 32 - NH && (32 * VEC + (lane - (32 - NH)) * VEC + VEC <= row_end);
+
+    auto issue = [&](int qi) {
+        if (qi < nq) {
+            const int q = z0 - R + qi;
+            const T* g = wrow + int64_t(q + a.order) * a.pitch;
+            T* r = ring + (qi % D) * SWR;
+            cp_async16(r + RA + lane * VEC, g + lane * VEC, c_ok);
+            if (q >= z0 && q < z1) {  // only output rows need the d1 halo
+                if (lane < NH) cp_async16(r + lane * VEC, g - RA + lane * VEC, true);
+                else if (lane >= 32 - NH) {
+                    const int k = lane - (32 - NH);
+                    cp_async16(r + RA + 32 * VEC + k * VEC, g + 32 * VEC + k * VEC, r_ok);
+                }
+            }
+        }
+        cp_async_commit();  // empty groups keep the wait count uniform
+    };
+
     P acc[NS][NPK];
 #pragma unroll
     for (int k = 0; k < NS; ++k)
 #pragma unroll
         for (int i = 0; i < NPK; ++i) acc[k][i] = K::mul(T(0), P{});
     P chk = K::mul(T(0), P{});
-    // rows in flight: a ring of D prefetched rows (left halo | centre | right halo);
-    // D divides the unroll factor NS so ring slots stay static registers
-    constexpr int D = 1;  // deeper rings (D = 3) cost occupancy and measured slower
-    T nx[D][VEC + 2 * RA];
-    auto fetch = [&](int qi_, T* dst) {
-        const int q_ = z0 - R + qi_;
-        const T* nrow = row0 + int64_t(q_ + a.order) * a.pitch;
-        ldg16(nrow, *reinterpret_cast<T(*)[VEC]>(&dst[RA]));
-        if (q_ >= z0 && q_ < z1) {
 #pragma unroll
-            for (int k = 0; k < RA / VEC; ++k) {
-                ldg16(nrow - RA + k * VEC, *reinterpret_cast<T(*)[VEC]>(&dst[k * VEC]));
-                ldg16(nrow + VEC + k * VEC, *reinterpret_cast<T(*)[VEC]>(&dst[RA + VEC + k * VEC]));
-            }
-        }
-    };
-#pragma unroll
-    for (int d = 0; d < D; ++d)
-        if (d < nq) fetch(d, nx[d]);
+    for (int d = 0; d < D - 1; ++d) issue(d);
 
     for (int qb = 0; qb < nq; qb += NS) {
 #pragma unroll
@@ -91,11 +128,14 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
             const int qi = qb + p;
             if (qi >= nq) break;
             const int q = z0 - R + qi;
-            // this row was fetched D steps ahead; refill its ring slot with row qi + D
+            __syncwarp();  // the slot refilled next was read by every lane last iteration
+            issue(qi + D - 1);
+            cp_async_wait<D - 1>();
+            __syncwarp();  // row qi of every lane has landed
+            const T* r = ring + (qi % D) * SWR + lane * VEC;
             T xr[VEC + 2 * RA];
 #pragma unroll
-            for (int i = 0; i < VEC + 2 * RA; ++i) xr[i] = nx[p % D][i];
-            if (qi + D < nq) fetch(qi + D, nx[p % D]);
+            for (int k = 0; k < (VEC + 2 * RA) / VEC; ++k) lds16(r + k * VEC, &xr[k * VEC]);
             P cv[NPK];
 #pragma unroll
             for (int k = 0; k < NPK; ++k) cv[k] = K::make(&xr[RA + k * W]);
@@ -143,36 +183,46 @@ __global__ void __launch_bounds__(128) star2d_kernel(const T* __restrict__ src, 
                     P o = acc[(p + NS - R) % NS][k];
                     if constexpr (DIV) o = K::mul(rdiv, o);
                     K::put(&v[k * W], o);
-                    chk = K::check(o, chk);
                 }
                 T* dp = out0 + int64_t(z + a.order) * a.pitch;
                 if (x_full) {
+#pragma unroll
+                    for (int k = 0; k < NPK; ++k) chk = K::check(K::make(&v[k * W]), chk);
                     stg16(dp, v);
                 } else {
 #pragma unroll
                     for (int i = 0; i < VEC; ++i)
-                        if (x + i >= a.lo1 && x + i < a.hi1) dp[i] = v[i];
+                        if (x + i >= a.lo1 && x + i < a.hi1) {
+                            dp[i] = v[i];
+                            chk = K::check(K::make(&v[i - i % W]), chk);
+                        }
                 }
             }
         }
     }
+    cp_async_wait<0>();
     if (__any_sync(0xffffffffu, !K::clean(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
 template <typename T, int R>
 cudaError_t launch2d_r(const Star2DArgs& a, const void* src, void* dst, bool div, cudaStream_t s) {
     const int warps = a.n_tx * a.n_tz;
-    const int blocks = (warps + 3) / 4;
+    const int blocks = (warps + Ring2D<T, R>::WARPS - 1) / Ring2D<T, R>::WARPS;
     Coef2D<T> cf;
     cf.c0 = T(a.c0);
     for (int m = 0; m < 4; ++m) {
         cf.cm0[m] = T(a.cm0[m]); cf.cp0[m] = T(a.cp0[m]); cf.cm1[m] = T(a.cm1[m]); cf.cp1[m] = T(a.cp1[m]);
     }
     cf.rdiv = T(a.rdiv);
-    if (div)
-        star2d_kernel<T, R, true><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
-    else
-        star2d_kernel<T, R, false><<<blocks, 128, 0, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
+    constexpr size_t smem = Ring2D<T, R>::SMEM;
+    auto kern = div ? star2d_kernel<T, R, true> : star2d_kernel<T, R, false>;
+    static bool attr_set[2] = {false, false};  // per instantiation pair
+    if (!attr_set[div]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr_set[div] = true;
+    }
+    kern<<<blocks, 32 * Ring2D<T, R>::WARPS, smem, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
     return cudaGetLastError();
 }
 
@@ -182,8 +232,10 @@ cudaError_t launch2d_t(Star2DArgs a, int R, const void* src, void* dst, bool div
     a.x0base = a.lo1 - (a.lo1 % VEC);
     a.n_tx = (a.hi1 - a.x0base + 32 * VEC - 1) / (32 * VEC);
     const int n0 = a.hi0 - a.lo0;
-    // enough warps to cover every SM several times; chunks no shorter than the halo
-    const int target = num_sms * 32;
+    // warps per SM to aim for (measured, 16384^2): short radii want many short chunks
+    // (balance), long radii fewer (each chunk re-streams 2R rows)
+    const int per_sm = R <= 2 ? 128 : (sizeof(T) == 8 || R == 3 ? 64 : 32);
+    const int target = num_sms * per_sm;
     int tz = (target + a.n_tx - 1) / a.n_tx;
     int lz = (n0 + tz - 1) / tz;
     if (lz < 2 * R) lz = 2 * R;

@@ -115,6 +115,8 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("STKB_BENCH_ONE_DEVICE"):  # tests only: every rank on cuda:0, gloo collectives
+        local = 0
     return ws, rank, local
 
 
@@ -200,8 +202,13 @@ def run_ours(args) -> None:
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("STKB_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")  # tests only (no NCCL between ranks sharing a GPU)
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     builder, shape, dtype, bpp, ref_name = CONFIGS[args.config]
+    if args.shape:  # tests only: a smaller grid of the same configuration
+        shape = tuple(int(x) for x in args.shape.split(","))
     if args.scaling == "weak":  # c4 weak scaling: (1024*G) x 1024 x 1024, fixed work per GPU
         shape = (shape[0] * ws,) + tuple(shape[1:])
     K, W = args.steps, args.warmup
@@ -249,7 +256,8 @@ def run_ours(args) -> None:
                         "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
                         "steps_per_call": K, "seconds": e["seconds"],
                         "what": "slabs.run_slab per rank: H2D of the rank's slabs from pinned host memory, "
-                                f"{K} steps with NCCL halo exchange, D2H; wall clock, max over ranks"}
+                                f"{K} steps with the {comm['transport']} halo exchange, D2H; wall clock, "
+                                "max over ranks"}
     if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
@@ -388,6 +396,7 @@ def main() -> None:
     ap.add_argument("--cpu-steps", type=int, default=30)
     ap.add_argument("--force-slabs", action="store_true",
                     help="use the z-slab/NCCL engine even on one GPU (tests the multi-GPU path)")
+    ap.add_argument("--shape", default=None, help=argparse.SUPPRESS)  # tests: smaller grid of the config
     ap.add_argument("--traffic", type=float, default=None,
                     help="DRAM bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()

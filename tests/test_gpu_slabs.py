@@ -201,3 +201,32 @@ def test_two_process_ipc_exchange_matches_unsplit_oracle(tmp_path, builder, shap
         got.interior[...] = np.concatenate([p[n][o:-o, o:-o, o:-o] for p in parts], axis=0)
         rep = compare(ref[n], got)
         assert rep.max_relative <= 1e-5, (n, rep.render())
+
+
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_bench_multi_rank_path_runs(scaling):
+    """bench.py's N>1 path (SlabBench + run_slab e2e, fused exchange over CUDA IPC) under
+    torchrun with two ranks sharing cuda:0 and gloo collectives: code-path check, not timing."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "4", "--warmup", "3", "--no-cpu", "--shape", "64,96,160", "--scaling", scaling]
+    env = dict(os.environ, STKB_BENCH_ONE_DEVICE="1")
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] >= 4
+    assert d["scaling"] == scaling
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["config"]["halo_exchange"]["transport"] == "p2p"

@@ -141,6 +141,16 @@ struct stkb_domain {
 
 namespace {
 
+// Step flags carry "launch v completed" as the bit pair {v mod 3, (v-1) mod 3}.  A
+// neighbour's completed count k stays within [c-2, c] while I wait to start launch c
+// (each launch waits for both neighbours' previous one), so the bit (c-1) mod 3 is set
+// exactly when k >= c-1.  The values a stream writes and waits for then repeat every
+// three launches, which lets a captured CUDA graph of the slab step be replayed.
+int32_t peer_mask(int32_t v) {
+    const int a = ((v % 3) + 3) % 3, b = (a + 2) % 3;
+    return (1 << a) | (1 << b);
+}
+
 // a 3-D tiled tensor map over one pitched grid buffer of `n0` interior planes
 int encode_tmap(stkb_domain* dom, void* base, int64_t n0, int bw, int bh, CUtensorMap* m) {
     int rc = get_encoder();
@@ -450,7 +460,10 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (cudaMalloc(&dom->d_flags, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
     cudaMemset(dom->d_flags, 0, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t));
     if (cudaMalloc(&dom->d_peer_flags, 2 * sizeof(int32_t)) != cudaSuccess) return cleanup("peer flags");
-    cudaMemset(dom->d_peer_flags, 0, 2 * sizeof(int32_t));
+    {
+        const int32_t done0[2] = {peer_mask(0), peer_mask(0)};  // "launch 0 completed"
+        cudaMemcpy(dom->d_peer_flags, done0, sizeof(done0), cudaMemcpyHostToDevice);
+    }
     if (const char* s = getenv("STKB_LZ")) dom->lz_override = atoi(s);
     if (const char* s = getenv("STKB_CTAS")) dom->ctas_override = atoi(s);
     if (const char* s = getenv("STKB_L2PROMO")) dom->l2promo = atoi(s);
@@ -1005,7 +1018,8 @@ int stkb_peer_signal(stkb_domain* dom, void* stream, int32_t value) {
         // I am my lower neighbour's upper neighbour (its slot 1) and vice versa;
         // the default flags fence this write after every prior store of the stream
         int32_t* slot = p.flags + (side == 0 ? 1 : 0);
-        CUresult r = write_fn(st, reinterpret_cast<CUdeviceptr>(slot), cuuint32_t(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+        CUresult r = write_fn(st, reinterpret_cast<CUdeviceptr>(slot), cuuint32_t(peer_mask(value)),
+                              CU_STREAM_WRITE_VALUE_DEFAULT);
         if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(int(r)));
     }
     return STKB_OK;
@@ -1019,8 +1033,8 @@ int stkb_peer_wait(stkb_domain* dom, void* stream, int32_t value) {
     CUstream st = static_cast<CUstream>(stream ? stream : dom->stream);
     for (int side = 0; side < 2; ++side) {
         if (!dom->peer[side].set) continue;
-        CUresult r = wait_fn(st, reinterpret_cast<CUdeviceptr>(dom->d_peer_flags + side), cuuint32_t(value),
-                             CU_STREAM_WAIT_VALUE_GEQ);
+        CUresult r = wait_fn(st, reinterpret_cast<CUdeviceptr>(dom->d_peer_flags + side),
+                             cuuint32_t(1u << (((value % 3) + 3) % 3)), CU_STREAM_WAIT_VALUE_AND);
         if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(int(r)));
     }
     return STKB_OK;

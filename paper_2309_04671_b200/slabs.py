@@ -22,6 +22,7 @@ and the sm_100a kernels (:class:`DeviceSlabEngine`).
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -239,8 +240,7 @@ def run_step_p2p(eng) -> None:
             eng.launch(i, 0, eng.plan.size)
             continue
         eng.t += 1
-        if eng.t > 1:
-            L.call("stkb_peer_wait", eng.dt.h, stream, ctypes.c_int32(eng.t - 1))
+        L.call("stkb_peer_wait", eng.dt.h, stream, ctypes.c_int32(eng.t - 1))
         L.call("stkb_launch_map_pull", eng.dt.h, eng.map_index[i])
         eng.launches += 1
         L.call("stkb_peer_signal", eng.dt.h, stream, ctypes.c_int32(eng.t))
@@ -286,6 +286,7 @@ class DeviceSlabEngine:
         self.launches = 0
         self.signal_target = {}  # map index -> running sum of its boundary signal
         self.t = 0  # exchanged launches issued (p2p flags)
+        self.graphs = {}  # (binding, t mod 3) -> (CUDA graph of graph_period() steps, launches, kernels)
         self._dist = None
         self.peers_connected = False
         streaming = all(p.kind in ("star", "wave", "box") for p in self.dt.plans) and len(decls_shape(decls)) == 3
@@ -383,6 +384,70 @@ class DeviceSlabEngine:
         else:
             run_step(self, dist, group)
 
+    def binding(self) -> tuple:
+        from . import _lib as L
+
+        out = []
+        for n in self.dt.names:
+            b = ctypes.c_int32()
+            L.call("stkb_binding", self.dt.h, self.dt.index[n], ctypes.byref(b))
+            out.append(b.value)
+        return tuple(out)
+
+    def graph_period(self) -> int:
+        """Steps after which both the name binding and the step-flag values (mod 3) repeat."""
+        names = list(self.dt.names)
+        bind = {n: n for n in names}
+        start = dict(bind)
+        bp = 0
+        while True:
+            for s in self.body:
+                if stmt_kind(s) == "BoundSwap":
+                    bind[s.first], bind[s.second] = bind[s.second], bind[s.first]
+            bp += 1
+            if bind == start:
+                break
+        maps = sum(1 for s in self.body if stmt_kind(s) == "BoundMap")
+        flag = 3 // math.gcd(maps, 3) if maps else 1
+        return bp * flag // math.gcd(bp, flag)
+
+    def run(self, n: int, dist=None) -> None:
+        """n time steps.  With the fused exchange the steps replay as CUDA graphs of
+        `graph_period()` steps (kernels and stream memory operations captured once per
+        starting binding), the remainder directly."""
+        import os
+
+        use = (self.transport == "p2p" and self.plan.world > 1 and self.peers_connected
+               and os.environ.get("STKB_SLAB_GRAPHS", "1") != "0")
+        if use:
+            torch = self.torch
+            period = self.graph_period()
+            while n >= period:
+                key = (self.binding(), self.t % 3)
+                hit = self.graphs.get(key)
+                if hit is None:
+                    # capture without a device synchronisation (other ranks' streams may be
+                    # waiting on this one): record `period` steps, which does not run them
+                    g = torch.cuda.CUDAGraph()
+                    t0, l0 = self.t, self.launches
+                    with torch.cuda.stream(self.compute):
+                        g.capture_begin(capture_error_mode="thread_local")
+                        try:
+                            for _ in range(period):
+                                run_step_p2p(self)  # host state (t, swaps) advances as if it had run
+                        finally:
+                            g.capture_end()
+                    hit = self.graphs[key] = (g, self.t - t0, self.launches - l0)
+                    self.t, self.launches = t0, l0
+                g, dt_, dl = hit
+                with torch.cuda.stream(self.compute):
+                    g.replay()
+                self.t += dt_
+                self.launches += dl
+                n -= period
+        for _ in range(n):
+            self.step(dist)
+
     def finish(self, halo: bool = True) -> None:
         """p2p: after the last step, wait for the neighbours' last launches and copy their
         boundary planes into this slab's halo planes (the slabs returned then match the NCCL
@@ -451,6 +516,7 @@ class DeviceSlabEngine:
         if getattr(self, "dt", None) is None:
             return
         self.torch.cuda.synchronize(self.dt.device)
+        self.graphs.clear()
         for p in self._ipc_opened:
             L.call("stkb_ipc_close", self.dt.device, ctypes.c_void_p(p))
         self._ipc_opened = []
@@ -521,8 +587,7 @@ def run_slab(bound, plan, local_grids: dict, slab: SlabPlan, dist, *, device: Op
         eng.dt.sync()
         if eng.transport == "p2p" and slab.world > 1:
             dist.barrier()  # every neighbour's slab is on its device before anyone reads it
-        for _ in range(count):
-            eng.step(dist)
+        eng.run(count, dist)
         eng.finish()
         eng.torch.cuda.synchronize()
         out = {}
@@ -624,8 +689,7 @@ class SlabBench:
         bench.fill_device(self.eng.dt, names, shp, builder, seed=7 + self.plan.rank)
 
     def warmup(self, w: int) -> None:
-        for _ in range(w):
-            self.eng.step(self.dist)
+        self.eng.run(w, self.dist)
         self.eng.finish(halo=False)
         self.torch.cuda.synchronize()
         self.dist.barrier()
@@ -637,8 +701,7 @@ class SlabBench:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         self.eng.launches = 0
         s.record(self.eng.compute)
-        for _ in range(k):
-            self.eng.step(self.dist)
+        self.eng.run(k, self.dist)
         self.eng.finish(halo=False)
         e.record(self.eng.compute)
         torch.cuda.synchronize()

@@ -7,7 +7,9 @@ from the real functions (with `_lib.call` replaced by a recorder) and
 replayed in many random interleavings, one in-order stream per rank, each
 kernel an interval [start, end].  Every interleaving must
 
-* never deadlock (a wait is eventually satisfied),
+* never deadlock (a wait is eventually satisfied) — with the real flag encoding: a wait
+  for launch v tests one bit of a word that only encodes the last two completions
+  (v mod 3), which is sound only while neighbours stay within one launch,
 * give each pulling launch c neighbour data exactly as a serial execution
   would (the neighbour's buffer was last written by its launch with the
   same index my own program last wrote it), and
@@ -86,10 +88,15 @@ def record_streams(body, names, world, steps, monkeypatch):
     return engines
 
 
-def simulate(engines, rng):
+def mask(v, mod=3):
+    """stkb200.cu peer_mask: "launch v completed" as the bit pair {v mod 3, (v-1) mod 3}."""
+    return (1 << (v % mod)) | (1 << ((v - 1) % mod))
+
+
+def simulate(engines, rng, mod=3):
     world = len(engines)
     pc = [0] * world  # next op per rank
-    flag = [0] * world  # value rank r last signalled to its neighbours
+    flag = [mask(0, mod)] * world  # flag word rank r last wrote into its neighbours (initial: launch 0 done)
     active = {}  # rank -> (reads, writes) of its running kernel
     version = [dict() for _ in range(world)]  # rank -> {buffer: index of its last writing launch}
     launches = [0] * world
@@ -103,7 +110,8 @@ def simulate(engines, rng):
             if pc[r] >= len(engines[r].ops):
                 continue
             op = engines[r].ops[pc[r]]
-            if op[0] == "wait" and not all(flag[n] >= op[1] for n in nbrs[r]):
+            # stream wait AND: the bit of launch v (only the last two completions are encoded)
+            if op[0] == "wait" and not all(flag[n] >> (op[1] % mod) & 1 for n in nbrs[r]):
                 continue
             moves.append(("op", r))
         if not moves:
@@ -118,8 +126,7 @@ def simulate(engines, rng):
         op = engines[r].ops[pc[r]]
         pc[r] += 1
         if op[0] == "signal":
-            assert op[1] >= flag[r]
-            flag[r] = op[1]
+            flag[r] = mask(op[1], mod)
         elif op[0] == "kernel":
             _, reads, writes = op
             launches[r] += 1
@@ -170,3 +177,13 @@ def test_protocol_checker_catches_a_missing_wait(monkeypatch):
     with pytest.raises(AssertionError):
         for _ in range(300):
             simulate(engines, rng)
+
+
+def test_protocol_checker_catches_a_too_short_flag_cycle(monkeypatch):
+    """Flags that encode launches mod 2 cannot tell 'one behind' from 'one ahead'."""
+    bound, decls = corpus.config_target("star3d4r_norm", (16, 16, 16), 1)
+    engines = record_streams(bound.stmts[0].body, list(decls), 3, steps=5, monkeypatch=monkeypatch)
+    rng = random.Random(11)
+    with pytest.raises(AssertionError):
+        for _ in range(300):
+            simulate(engines, rng, mod=2)

@@ -75,13 +75,11 @@ def main():
     local = (plan.size,) + tuple(shape[1:])
     bench.fill_device(eng.dt, list(decls), local, builder)
     d = NullDist()
-    for _ in range(3):
-        eng.step(d)
+    eng.run(2 * eng.graph_period() if transport == "p2p" else 3, d)  # warm-up (captures the step graph)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(eng.compute)
-    for _ in range(steps):
-        eng.step(d)
+    eng.run(steps, d)
     e.record(eng.compute)
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps

@@ -177,8 +177,11 @@ int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (le
  * (both neighbours finished launch c-1: the planes I read are final) and
  * stkb_peer_signal(c) (a fenced stream write into each neighbour's flag, so a
  * neighbour's launch c+1 cannot overwrite planes my launch c still reads) —
- * stream memory operations only: no kernel ever waits on another.
- * stkb_peer_fetch_halo copies the neighbours' boundary planes into this
+ * stream memory operations only: no kernel ever waits on another.  A flag word
+ * encodes "launch v done" as the bits {v mod 3, (v-1) mod 3}, so the values repeat
+ * every three launches and a captured CUDA graph of the step can be replayed;
+ * callers must keep the launch count identical on every rank (one counted launch
+ * per map per step).  stkb_peer_fetch_halo copies the neighbours' boundary planes into this
  * slab's halo planes (after the last step, to return consistent slabs). */
 int stkb_launch_map_pull(stkb_domain *dom, int32_t map_index);
 int stkb_peer_fetch_halo(stkb_domain *dom, void *stream, int32_t planes);

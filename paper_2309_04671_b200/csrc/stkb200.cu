@@ -518,6 +518,20 @@ int stkb_set_stream(stkb_domain* dom, void* stream) {
     return STKB_OK;
 }
 
+// A pitched cudaMemcpy2D runs at ~60 % of PCIe speed on B200 hosts; transfers go
+// through a device staging buffer in contiguous chunks, repitched on the device.
+static bool ensure_stage(stkb_domain* dom, size_t want) {
+    constexpr size_t kStage = size_t(256) << 20;
+    if (!dom->d_stage) {
+        dom->stage_bytes = std::min(kStage, want);
+        if (cudaMalloc(&dom->d_stage, dom->stage_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            dom->d_stage = nullptr;
+        }
+    }
+    return dom->d_stage != nullptr;
+}
+
 static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
     if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_upload")) return rc;
@@ -526,17 +540,7 @@ static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
     const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
     const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
     char* dst = static_cast<char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
-    // A pitched cudaMemcpy2D runs at ~60 % of PCIe speed on B200 hosts; copy
-    // contiguous chunks into a staging buffer instead and repitch on the device.
-    constexpr size_t kStage = size_t(256) << 20;
-    if (!dom->d_stage) {
-        dom->stage_bytes = std::min(kStage, rows * row);
-        if (cudaMalloc(&dom->d_stage, dom->stage_bytes) != cudaSuccess) {
-            cudaGetLastError();
-            dom->d_stage = nullptr;
-        }
-    }
-    if (!dom->d_stage) {  // no memory for staging: direct pitched copy
+    if (!ensure_stage(dom, rows * row)) {  // no memory for staging: direct pitched copy
         CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(g.pitch) * dom->elem, host, row, row, rows, cudaMemcpyHostToDevice,
                                    dom->stream));
         return STKB_OK;
@@ -558,10 +562,21 @@ static int copy_d2h(stkb_domain* dom, int32_t name, void* host) {
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     const Geometry& g = dom->g;
     const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
+    const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
     const char* src = static_cast<const char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
-    CUDA_TRY(cudaMemcpy2DAsync(host, row, src, size_t(g.pitch) * dom->elem, row,
-                               size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order), cudaMemcpyDeviceToHost,
-                               dom->stream));
+    if (!ensure_stage(dom, rows * row)) {
+        CUDA_TRY(cudaMemcpy2DAsync(host, row, src, size_t(g.pitch) * dom->elem, row, rows, cudaMemcpyDeviceToHost,
+                                   dom->stream));
+        return STKB_OK;
+    }
+    const size_t chunk_rows = std::max<size_t>(1, dom->stage_bytes / row);
+    char* out = static_cast<char*>(host);
+    for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+        const size_t nr = std::min(chunk_rows, rows - r0);
+        CUDA_TRY(launch_repitch(src + r0 * size_t(g.pitch) * dom->elem, dom->d_stage, int64_t(nr), int64_t(row),
+                                int64_t(g.pitch) * int64_t(dom->elem), int64_t(row), dom->num_sms, dom->stream));
+        CUDA_TRY(cudaMemcpyAsync(out + r0 * row, dom->d_stage, nr * row, cudaMemcpyDeviceToHost, dom->stream));
+    }
     return STKB_OK;
 }
 

@@ -133,7 +133,7 @@ struct stkb_domain {
     size_t stage_bytes = 0;
     int lz_override = 0;
     int ctas_override = 0;
-    int l2promo = 3;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
+    int l2promo = 2;      // tensor-map L2 promotion (STKB_L2PROMO: 0 none, 1 64B, 2 128B (measured best), 3 256B)
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
     bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
     int order_y_fast = 0; // STKB_ORDER_Y=1: work items walk y tiles fastest

@@ -393,7 +393,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=30)
+    ap.add_argument("--cpu-steps", type=int, default=300,
+                    help="time steps of the bounded CPU-baseline sample (~10 s of CPU work for c4)")
     ap.add_argument("--force-slabs", action="store_true",
                     help="use the z-slab/NCCL engine even on one GPU (tests the multi-GPU path)")
     ap.add_argument("--shape", default=None, help=argparse.SUPPRESS)  # tests: smaller grid of the config

@@ -127,6 +127,7 @@ int stkb_layout(const stkb_domain *dom, int64_t *pitch_elems, int64_t *plane_ele
                 int64_t *lead_elems, int64_t *buffer_elems);
 int stkb_device_ptr(stkb_domain *dom, int32_t name, void **dptr);
 int stkb_set_stream(stkb_domain *dom, void *cuda_stream); /* NULL = domain's own */
+int stkb_zero(stkb_domain *dom, int32_t name);            /* whole buffer (halo, padding) = 0, async */
 
 /* host <-> device, GridBuffer.data layout (C-order, padded, unpitched) */
 int stkb_upload(stkb_domain *dom, int32_t name, const void *host_padded);

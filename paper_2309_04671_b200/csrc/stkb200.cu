@@ -512,6 +512,15 @@ int stkb_device_ptr(stkb_domain* dom, int32_t name, void** dptr) {
     return STKB_OK;
 }
 
+int stkb_zero(stkb_domain* dom, int32_t name) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (int rc = check_name(dom, name, "stkb_zero")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
+    CUDA_TRY(cudaMemsetAsync(dom->bufs[dom->binding[name]], 0, bytes, dom->stream));
+    return STKB_OK;
+}
+
 int stkb_set_stream(stkb_domain* dom, void* stream) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     dom->stream = stream ? static_cast<cudaStream_t>(stream) : dom->own_stream;

@@ -340,3 +340,31 @@ def test_fast_path_linearity_within_4ulp():
     b = o2["u"].interior.astype(np.float64)
     rel = np.abs(a - b) / np.maximum(np.abs(a), np.finfo(np.float32).tiny)
     assert rel.max() <= 4 * np.finfo(np.float32).eps
+
+
+def test_reused_device_domain_is_clean():
+    """run_gpu keeps its device domain for the next call of the same layout; a reused
+    domain must not leak the previous call's data (here: a non-zero halo left in the
+    buffer a dead, zero-halo input is skipped into) and must give the same results."""
+    from paper_2309_04671_b200 import release_device_cache
+    from paper_2309_04671_b200.backend import LAST_RUN
+
+    bound, decls = corpus.config_target("star3d2r", (20, 24, 40), 3)
+    first = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(first["u"], 3)
+    first["v"].data[...] = 7.25  # non-zero halo: uploaded, and left on the device
+    release_device_cache()
+    run_gpu(bound, _plan(bound), first, precision="exact")
+    assert LAST_RUN["reused_domain"] is False
+    second = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(second["u"], 4)
+    ref = oracle.run_target_c(bound, second)
+    got = run_gpu(bound, _plan(bound), second, precision="exact")
+    assert LAST_RUN["reused_domain"] is True
+    assert LAST_RUN["h2d_bytes"] == second["u"].data.nbytes  # v skipped (dead, zero halo)
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), n
+    again = run_gpu(bound, _plan(bound), second)  # fast path on the same reused domain
+    for n in ref:
+        assert compare(ref[n], again[n]).max_relative <= 1e-5, n
+    release_device_cache()

@@ -475,8 +475,9 @@ class DeviceSlabEngine:
     def connect_ipc(self, dist) -> None:
         """Exchange CUDA IPC handles with the z-neighbours and map their buffers.
 
-        If any rank cannot reach a neighbour's GPU (no peer access), every rank falls
-        back to the NCCL transport together (the decision is collective)."""
+        If any rank cannot reach a neighbour's GPU (no peer access) or fails to map a
+        neighbour's memory, every rank falls back to the NCCL transport together (both
+        decisions are collective, so no rank is left waiting on a flag)."""
         from . import _lib as L
 
         self._dist = dist
@@ -485,30 +486,41 @@ class DeviceSlabEngine:
         every = [None] * self.plan.world
         dist.all_gather_object(every, mine)
         ok = all(self._can_reach(every[p]["uuid"]) for p in (self.plan.lower, self.plan.upper) if p is not None)
+        why = "z-slab neighbours without peer access"
+        if ok:
+            try:
+                for side, peer in ((0, self.plan.lower), (1, self.plan.upper)):
+                    if peer is None:
+                        continue
+                    info = every[peer]
+                    ptrs = []
+                    for raw in info["bufs"] + [info["flags"]]:
+                        p = ctypes.c_void_p()
+                        L.call("stkb_ipc_open", self.dt.device, ctypes.create_string_buffer(raw, 64),
+                               ctypes.byref(p))
+                        ptrs.append(p.value)
+                        self._ipc_opened.append(p.value)
+                    arr = (ctypes.c_void_p * (len(ptrs) - 1))(*ptrs[:-1])
+                    L.call("stkb_set_peer", self.dt.h, side, len(ptrs) - 1, arr, ctypes.c_void_p(ptrs[-1]),
+                           ctypes.c_int64(info["n0"]))
+            except L.StkbError as exc:
+                ok, why = False, f"mapping a neighbour's memory failed ({exc})"
         votes = [None] * self.plan.world
         dist.all_gather_object(votes, ok)
-        if not all(votes):
-            import warnings
-
-            warnings.warn("z-slab neighbours without peer access: halo exchange falls back to NCCL")
-            self.transport = "nccl"
-            self._reserve_nccl_sms()
-            self._dist = None
+        if all(votes):
+            self.peers_connected = True
             return
-        for side, peer in ((0, self.plan.lower), (1, self.plan.upper)):
-            if peer is None:
-                continue
-            info = every[peer]
-            ptrs = []
-            for raw in info["bufs"] + [info["flags"]]:
-                p = ctypes.c_void_p()
-                L.call("stkb_ipc_open", self.dt.device, ctypes.create_string_buffer(raw, 64), ctypes.byref(p))
-                ptrs.append(p.value)
-                self._ipc_opened.append(p.value)
-            arr = (ctypes.c_void_p * (len(ptrs) - 1))(*ptrs[:-1])
-            L.call("stkb_set_peer", self.dt.h, side, len(ptrs) - 1, arr, ctypes.c_void_p(ptrs[-1]),
-                   ctypes.c_int64(info["n0"]))
-        self.peers_connected = True
+        import warnings
+
+        warnings.warn(f"{why}: the z-slab halo exchange falls back to NCCL on every rank")
+        for side in (0, 1):
+            L.call("stkb_set_peer", self.dt.h, side, 0, None, None, ctypes.c_int64(0))
+        for p in self._ipc_opened:
+            L.call("stkb_ipc_close", self.dt.device, ctypes.c_void_p(p))
+        self._ipc_opened = []
+        self.transport = "nccl"
+        self._reserve_nccl_sms()
+        self._dist = None
 
     def close(self):
         from . import _lib as L

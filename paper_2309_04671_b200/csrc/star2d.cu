@@ -24,12 +24,15 @@ struct Star2DArgs {
     int32_t* nonfinite;
     double c0, cm0[4], cp0[4], cm1[4], cp1[4];  // d0 / d1 coefficients (offset -m / +m)
     double rdiv;     // 1/divisor or 0
+    int32_t box;     // dense (2R+1)^2 coefficient square instead of the star
+    double cb[81];   // box: cb[(dy+R)*(2R+1) + (dx+R)]
 };
 
 // the same coefficients in the grid dtype, read straight from the parameter bank
 template <typename T>
 struct Coef2D {
     T c0, cm0[4], cp0[4], cm1[4], cp1[4], rdiv;
+    T cb[81];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -59,7 +62,7 @@ struct Ring2D {
     static constexpr size_t SMEM = size_t(WARPS) * D * SWR * sizeof(T);
 };
 
-template <typename T, int R, bool DIV>
+template <typename T, int R, bool DIV, bool BOX>
 __global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __restrict__ src, T* __restrict__ dst,
                                                      const __grid_constant__ Star2DArgs a,
                                                      const __grid_constant__ Coef2D<T> cf) {
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __r
             const T* g = wrow + int64_t(q + a.order) * a.pitch;
             T* r = ring + (qi % D) * SWR;
             cp_async16(r + RA + lane * VEC, g + lane * VEC, c_ok);
-            if (q >= z0 && q < z1) {  // only output rows need the d1 halo
+            if (BOX || (q >= z0 && q < z1)) {  // star: only output rows need the d1 halo
                 if (lane < NH) cp_async16(r + lane * VEC, g - RA + lane * VEC, true);
                 else if (lane >= 32 - NH) {
                     const int k = lane - (32 - NH);
@@ -139,6 +142,24 @@ __global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __r
             P cv[NPK];
 #pragma unroll
             for (int k = 0; k < NPK; ++k) cv[k] = K::make(&xr[RA + k * W]);
+            if constexpr (BOX) {
+                // row q adds its layer dy of the (2R+1)^2 square to output row q - dy; the
+                // dy = -R layer is the first one output q + R receives (it initialises the slot)
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+                    constexpr int NW = 2 * R + 1;
+                    const int slot = (p - dy + 2 * NS) % NS;
+#pragma unroll
+                    for (int k = 0; k < NPK; ++k) {
+                        P s_ = dy == -R ? K::mul(cf.cb[(dy + R) * NW], K::make(&xr[RA + k * W - R]))
+                                        : K::fma(cf.cb[(dy + R) * NW], K::make(&xr[RA + k * W - R]), acc[slot][k]);
+#pragma unroll
+                        for (int dx = -R + 1; dx <= R; ++dx)
+                            s_ = K::fma(cf.cb[(dy + R) * NW + dx + R], K::make(&xr[RA + k * W + dx]), s_);
+                        acc[slot][k] = s_;
+                    }
+                }
+            } else {
             if (q >= z0 && q < z1) {
 #pragma unroll
                 for (int k = 0; k < NPK; ++k) {
@@ -175,6 +196,7 @@ __global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __r
 #pragma unroll
                 for (int m = 1; m <= R; ++m)
                     acc[(p - m + NS) % NS][k] = K::fma(cpz[m - 1], cv[k], acc[(p - m + NS) % NS][k]);
+            }  // star
             const int z = q - R;
             if (z >= z0 && z < z1 && x_any) {
                 T v[VEC];
@@ -204,18 +226,12 @@ __global__ void __launch_bounds__(32 * STKB_2D_WARPS) star2d_kernel(const T* __r
     if (__any_sync(0xffffffffu, !K::clean(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
-template <typename T, int R>
-cudaError_t launch2d_r(const Star2DArgs& a, const void* src, void* dst, bool div, cudaStream_t s) {
+template <typename T, int R, bool BOX>
+cudaError_t launch2d_rb(const Star2DArgs& a, const Coef2D<T>& cf, const void* src, void* dst, bool div, cudaStream_t s) {
     const int warps = a.n_tx * a.n_tz;
     const int blocks = (warps + Ring2D<T, R>::WARPS - 1) / Ring2D<T, R>::WARPS;
-    Coef2D<T> cf;
-    cf.c0 = T(a.c0);
-    for (int m = 0; m < 4; ++m) {
-        cf.cm0[m] = T(a.cm0[m]); cf.cp0[m] = T(a.cp0[m]); cf.cm1[m] = T(a.cm1[m]); cf.cp1[m] = T(a.cp1[m]);
-    }
-    cf.rdiv = T(a.rdiv);
     constexpr size_t smem = Ring2D<T, R>::SMEM;
-    auto kern = div ? star2d_kernel<T, R, true> : star2d_kernel<T, R, false>;
+    auto kern = div ? star2d_kernel<T, R, true, BOX> : star2d_kernel<T, R, false, BOX>;
     static bool attr_set[2] = {false, false};  // per instantiation pair
     if (!attr_set[div]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -224,6 +240,19 @@ cudaError_t launch2d_r(const Star2DArgs& a, const void* src, void* dst, bool div
     }
     kern<<<blocks, 32 * Ring2D<T, R>::WARPS, smem, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
     return cudaGetLastError();
+}
+
+template <typename T, int R>
+cudaError_t launch2d_r(const Star2DArgs& a, const void* src, void* dst, bool div, cudaStream_t s) {
+    Coef2D<T> cf;
+    cf.c0 = T(a.c0);
+    for (int m = 0; m < 4; ++m) {
+        cf.cm0[m] = T(a.cm0[m]); cf.cp0[m] = T(a.cp0[m]); cf.cm1[m] = T(a.cm1[m]); cf.cp1[m] = T(a.cp1[m]);
+    }
+    cf.rdiv = T(a.rdiv);
+    for (int i = 0; i < 81; ++i) cf.cb[i] = T(a.cb[i]);
+    if (a.box) return launch2d_rb<T, R, true>(a, cf, src, dst, div, s);
+    return launch2d_rb<T, R, false>(a, cf, src, dst, div, s);
 }
 
 template <typename T>

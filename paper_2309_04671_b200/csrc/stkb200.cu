@@ -40,6 +40,8 @@ struct Star2DArgs {
     int32_t* nonfinite;
     double c0, cm0[4], cp0[4], cm1[4], cp1[4];
     double rdiv;
+    int32_t box;
+    double cb[81];
 };
 cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
                           cudaStream_t s);
@@ -229,6 +231,10 @@ int launch_star2d_map(stkb_domain* dom, const MapOp& op, const std::vector<int32
         a.cp1[m - 1] = m <= R ? d.coef[1 + 2 * R + 2 * (m - 1) + 1] : 0.0;
     }
     a.rdiv = d.divisor != 0.0 ? 1.0 / d.divisor : 0.0;
+    if (d.kind == STKB_MAP_BOX) {
+        a.box = 1;
+        for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) a.cb[i] = d.box_coef[i];
+    }
     cudaError_t e = launch_star2d(dom->desc.dtype, a, R, dom->bufs[bind[d.src]], dom->bufs[bind[d.dst]],
                                   d.divisor != 0.0, dom->num_sms, dom->stream);
     if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("2-D star kernel launch: ") + cudaGetErrorString(e));
@@ -640,10 +646,11 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     op.d = d;
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
     if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX) {
-        if (nd != 3 && !(nd == 2 && d.kind == STKB_MAP_STAR))
-            return fail(STKB_ERR_UNSUPPORTED, "2-D grids stream star maps only");
+        if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
+            return fail(STKB_ERR_UNSUPPORTED, "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
-        if (d.kind == STKB_MAP_BOX && d.radius > 2) return fail(STKB_ERR_UNSUPPORTED, "streaming box kernels cover radius 1..2");
+        if (d.kind == STKB_MAP_BOX && nd == 3 && d.radius > 2)
+            return fail(STKB_ERR_UNSUPPORTED, "3-D streaming box kernels cover radius 1..2");
         if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");
         if (int rc = check_name(dom, d.src, "src")) return rc;
         if (int rc = check_name(dom, d.dst, "dst")) return rc;

@@ -193,7 +193,17 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
         offs = [k[0][1] for k in deg1]
         r = max(max(abs(c) for c in o) for o in offs)
         if dims == 2 and not _is_star(offs, 2):
-            raise MatchError("2-D box/other shape")
+            if r < 1 or r > MAX_FAST_RADIUS:
+                raise MatchError(f"2-D box/other shape of radius {r} outside 1..{MAX_FAST_RADIUS}")
+            src = params[src_param]
+            if src == dst:
+                raise MatchError("in-place update (reads and writes the same grid)")
+            n = 2 * r + 1
+            square = [0.0] * n * n
+            for k, v in deg1.items():
+                dy, dx = k[0][1]
+                square[(dy + r) * n + (dx + r)] = v
+            return MapPlan("box", r, src, dst, coef=square, divisor=divisor, box=box)
         if dims == 3 and not _is_star(offs, 3):
             if r > MAX_BOX_RADIUS:
                 raise MatchError(f"box/other shape of radius {r} (dense streaming kernel covers <= {MAX_BOX_RADIUS})")

@@ -62,7 +62,8 @@ def test_library_rejects_bad_descriptors_without_gpu():
                                           ("star3d3r", "star"), ("star3d4r_norm", "star"), ("jacobi7", "star"),
                                           ("wave", "wave"), ("j3d27pt", "box"), ("box3d2r", "box"),
                                           ("box3d1r", "box"), ("box3d3r", "expr"), ("star2d4r", "star"),
-                                          ("j2d5pt", "star"), ("box2d1r", "expr")])
+                                          ("j2d5pt", "star"), ("box2d1r", "box"), ("box2d4r", "box"),
+                                          ("j2d9pt_gol", "box")])
 def test_matcher_routes(builder, kind):
     shape = (16, 16) if corpus.KERNELS.get(builder) and corpus.KERNELS[builder].dims == 2 else (16, 16, 16)
     bound, _ = corpus.config_target(builder, shape, 1)

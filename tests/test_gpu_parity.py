@@ -89,7 +89,8 @@ def test_fast_ragged_and_c1_shapes_vs_c_oracle(shape, dtype, kernel):
 
 @pytest.mark.parametrize("shape,dtype", [((1000, 1000), "f32"), ((37, 133), "f32"), ((9, 700), "f32"),
                                          ((130, 257), "f64")])
-@pytest.mark.parametrize("kernel", ["star2d4r", "star2d1r", "j2d5pt", "j2d9pt", "star2d3r"])
+@pytest.mark.parametrize("kernel", ["star2d4r", "star2d1r", "j2d5pt", "j2d9pt", "star2d3r", "box2d1r", "box2d2r",
+                                    "box2d3r", "box2d4r", "j2d9pt_gol"])
 def test_fast_2d_streaming_vs_c_oracle(shape, dtype, kernel):
     bound, decls = corpus.config_target(kernel, shape, 5, dtype)
     grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}

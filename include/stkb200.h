@@ -111,8 +111,11 @@ typedef struct {
     const int32_t *code;
     int32_t n_consts;
     const double *consts;
-    /* BOX only: box_coef[((dz+R)*(2R+1) + (dy+R))*(2R+1) + (dx+R)] */
+    /* BOX only: box_coef[((dz+R)*(2R+1) + (dy+R))*(2R+1) + (dx+R)] (3-D, R <= 2) or
+     * box_coef[(dy+R)*(2R+1) + (dx+R)] (2-D, R <= 4) */
     double box_coef[125];
+    /* BOX, 3-D, R = 3..4: the (2R+1)^3 coefficients in the same order (copied at add_map) */
+    const double *box_coef_ext;
 } stkb_map_desc;
 
 /* library */

@@ -74,6 +74,7 @@ class MapDesc(ctypes.Structure):
         ("n_consts", ctypes.c_int32),
         ("consts", ctypes.POINTER(ctypes.c_double)),
         ("box_coef", ctypes.c_double * 125),
+        ("box_coef_ext", ctypes.POINTER(ctypes.c_double)),
     ]
 
 

@@ -197,11 +197,16 @@ class DeviceTarget:
             if plan.kind == "wave":
                 d.prev, d.vel = self.index[plan.prev], self.index[plan.vel]
                 d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
-            for i, c in enumerate(plan.coef):
-                if plan.kind == "box":
-                    d.box_coef[i] = c
-                else:
-                    d.coef[i] = c
+            if plan.kind == "box" and len(plan.coef) > 125:  # 3-D box of radius 3..4
+                ext = np.ascontiguousarray(np.array(plan.coef, dtype=np.float64))
+                d._keep_ext = ext  # alive until stkb_program_add_map has copied it
+                d.box_coef_ext = ext.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            else:
+                for i, c in enumerate(plan.coef):
+                    if plan.kind == "box":
+                        d.box_coef[i] = c
+                    else:
+                        d.coef[i] = c
             d.divisor = plan.divisor
         else:
             d.kind = L.STKB_MAP_EXPR

@@ -53,7 +53,6 @@ struct StarArgs {
     T cp[3][4];                // [axis][m-1] coefficient of offset +m
     T divisor;
     T wave_a, wave_b;
-    T cb[125];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 2
     int32_t store_hint;        // 1: streaming (evict-first) output stores
     int32_t order_y_fast;      // work items walk y tiles fastest
     // fused halo exchange (multi-GPU z-slabs): src planes q < 0 are read by TMA
@@ -62,6 +61,8 @@ struct StarArgs {
     // when bit 1 is — over NVLink, in place of this slab's own halo planes
     int32_t pull;
     int32_t pull_lo_n0;
+    T cb[729];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 4 (last: the
+                               // other fields keep their parameter-bank offsets)
 };
 
 // ---------------------------------------------------------------------------

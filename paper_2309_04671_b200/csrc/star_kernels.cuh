@@ -298,9 +298,14 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         // output address of row jr0 at plane z: dst0 + (z + order0) * plane + j * pitch
         T* const dst0 = a.dst + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x;
 
-        for (int qb = 0; qb < nq; qb += NS) {
+        // the plane loop is unrolled by 2R+1 so the accumulator ring slots are static
+        // registers; the wide dense boxes (R > 2: 343 / 729 taps per plane) keep one plane
+        // per iteration (code size) and rotate the ring instead (2R+1 register moves)
+        constexpr bool ROT = (FORM == FORM_BOX || FORM == FORM_BOX_DIV) && R > 2;
+        constexpr int PU = ROT ? 1 : NS;
+        for (int qb = 0; qb < nq; qb += PU) {
 #pragma unroll
-            for (int p = 0; p < NS; ++p) {
+            for (int p = 0; p < PU; ++p) {
                 const int qi = qb + p;
                 if (qi < nq) {
                     const int q = z0 - R + qi;
@@ -502,6 +507,18 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                             }
                         }
                     }
+                    if constexpr (ROT) {
+                        // output o lives in slot (o - q) mod NS: move every slot down by one
+#pragma unroll
+                        for (int j = 0; j < TY; ++j)
+#pragma unroll
+                            for (int k = 0; k < NPK; ++k) {
+                                const P first = acc[0][j][k];
+#pragma unroll
+                                for (int r = 0; r + 1 < NS; ++r) acc[r][j][k] = acc[r + 1][j][k];
+                                acc[NS - 1][j][k] = first;
+                            }
+                    }
                 }
             }
         }
@@ -651,7 +668,10 @@ __host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = f
         case 7: return Variant{2, 12, true};
         case 8: return Variant{3, 8, true};
         default:  // measured best on B200 per form, dtype and radius (tools/sweep.py)
-            if (box) return Variant{R == 1 ? 4 : 1, 15, true};  // dense cube (R=2: 125 taps, one row per warp)
+            // dense cubes: R=1 4 rows/warp (rows share taps), R=2 one row, R=3..4 one row with
+            // 11 warps (up to 170 registers); R=4 forms odd-shift pairs once per row (+13 %)
+            if (box) return R == 1 ? Variant{4, 15, true} : (R <= 3 ? Variant{1, R == 2 ? 15 : 11, true}
+                                                                    : Variant{1, 11, false});
             if (R == 1) return Variant{1, 15, true};
             if (R == 2) return sizeof(T) == 8 ? Variant{2, 9, true} : Variant{1, 15, true};
             return Variant{2, 11, true};
@@ -671,13 +691,11 @@ template <typename T, int R, int V, bool PULL>
 cudaError_t launch_star_vp(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
     constexpr Variant vv = star_variant_of<T>(R, V);
     if (L.kind == 4) {
-        if constexpr (R <= 2) {
+        {
             constexpr Variant vb = star_variant_of<T>(R, V, true);
             if (L.has_divisor)
                 return launch_star_cfg<T, R, FORM_BOX_DIV, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
             return launch_star_cfg<T, R, FORM_BOX, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
-        } else {
-            return cudaErrorInvalidValue;
         }
     }
     if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);

@@ -76,6 +76,7 @@ struct MapOp {
     int32_t* d_code = nullptr;
     double* d_consts = nullptr;
     bool snapshot[STKB_EXPR_MAX_ARGS] = {};  // EXPR: arg written and read -> read a copy
+    std::vector<double> cube;                // BOX: the (2R+1)^3 coefficients (any R)
 };
 
 struct ProgOp {
@@ -279,7 +280,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.store_hint = dom->store_hint;
     a.order_y_fast = dom->order_y_fast;
     if (d.kind == STKB_MAP_BOX)
-        for (int i = 0; i < 125; ++i) a.cb[i] = T(d.box_coef[i]);
+        for (size_t i = 0; i < op.cube.size(); ++i) a.cb[i] = T(op.cube[i]);
 
     int bx, by, hx;
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
@@ -649,8 +650,14 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
             return fail(STKB_ERR_UNSUPPORTED, "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
-        if (d.kind == STKB_MAP_BOX && nd == 3 && d.radius > 2)
-            return fail(STKB_ERR_UNSUPPORTED, "3-D streaming box kernels cover radius 1..2");
+        if (d.kind == STKB_MAP_BOX && nd == 3) {
+            const int n = 2 * d.radius + 1;
+            if (d.radius > 2 && !d.box_coef_ext)
+                return fail(STKB_ERR_ARG, "a 3-D box map of radius > 2 passes its coefficients in box_coef_ext");
+            const double* src = d.radius > 2 ? d.box_coef_ext : d.box_coef;
+            op.cube.assign(src, src + size_t(n) * n * n);
+        }
+        op.d.box_coef_ext = nullptr;  // copied: the caller's array need not outlive this call
         if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");
         if (int rc = check_name(dom, d.src, "src")) return rc;
         if (int rc = check_name(dom, d.dst, "dst")) return rc;

@@ -24,7 +24,7 @@ from typing import Optional
 from .program import node_kind
 
 MAX_FAST_RADIUS = 4
-MAX_BOX_RADIUS = 2
+MAX_BOX_RADIUS = 4
 
 
 class MatchError(ValueError):

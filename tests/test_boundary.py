@@ -61,7 +61,7 @@ def test_library_rejects_bad_descriptors_without_gpu():
 @pytest.mark.parametrize("builder,kind", [("star3d4r", "star"), ("star3d1r", "star"), ("star3d2r", "star"),
                                           ("star3d3r", "star"), ("star3d4r_norm", "star"), ("jacobi7", "star"),
                                           ("wave", "wave"), ("j3d27pt", "box"), ("box3d2r", "box"),
-                                          ("box3d1r", "box"), ("box3d3r", "expr"), ("star2d4r", "star"),
+                                          ("box3d1r", "box"), ("box3d3r", "box"), ("box3d4r", "box"), ("star2d4r", "star"),
                                           ("j2d5pt", "star"), ("box2d1r", "box"), ("box2d4r", "box"),
                                           ("j2d9pt_gol", "box")])
 def test_matcher_routes(builder, kind):

@@ -103,7 +103,7 @@ def test_fast_2d_streaming_vs_c_oracle(shape, dtype, kernel):
 
 
 @pytest.mark.parametrize("shape,dtype", [((37, 45, 133), "f32"), ((64, 64, 64), "f32"), ((21, 38, 70), "f64")])
-@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r"])
+@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r", "box3d3r", "box3d4r"])
 def test_fast_box_kernels_vs_c_oracle(shape, dtype, kernel):
     bound, decls = corpus.config_target(kernel, shape, 3, dtype)
     grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}

@@ -130,6 +130,23 @@ def test_region_maps_vs_c_oracle(width, scheme):
                 assert compare(ref[n], got[n]).max_relative <= 1e-5
 
 
+@pytest.mark.parametrize("width,scheme", [(4, "cross_product"), (6, "slab7")])
+def test_wave_with_pml_regions_vs_c_oracle(width, scheme):
+    """The acoustic ISO workload's region split (PML boundary layers) on the
+    wave form: one streaming launch over the exact-cover box per map, bitwise on the exact path."""
+    bound, decls = corpus.wave_target((40, 44, 80), 6, "f32", 4, width, scheme)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    corpus.wave_inputs(grids)
+    ref = oracle.run_target_c(bound, grids)
+    for precision in ("fast", "exact"):
+        got = run_gpu(bound, _plan(bound), grids, precision=precision)
+        for n in ref:
+            if precision == "exact":
+                assert np.array_equal(ref[n].data, got[n].data), n
+            else:
+                assert compare(ref[n], got[n]).max_relative <= 1e-5, (n, compare(ref[n], got[n]).render())
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_wave_c3_form_vs_c_oracle(dtype):
     bound, decls = corpus.wave_target((64, 72, 96), 20, dtype)

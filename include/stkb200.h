@@ -168,6 +168,16 @@ int stkb_launch_map_ranges(stkb_domain *dom, int32_t map_index, int32_t n_ranges
 int stkb_stream_wait_signal(stkb_domain *dom, void *stream, int32_t map_index, int32_t value);
 int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (leave SMs for NCCL) */
 
+/* Two time steps per d0 sweep (temporal blocking, on by default): when the step
+ * program is the Jacobi ping-pong `v = S(u); swap(u, v)` of a fast 3-D STAR map of
+ * radius <= 2 (executor.py:267-286 semantics), stkb_run of n >= 4 steps runs
+ * (n - 2) / 2 fused sweeps u(t+2) = S(S(u(t))) — v(t+1) stays in registers — and
+ * the last 2..3 steps singly, so every grid ends with exactly the single-step
+ * kernel's values (bit for bit; the fused sweep keeps each step's FMA order).  It
+ * allocates one scratch grid; u's name rotates between its buffer and the scratch
+ * (stkb_binding may then report buffer index n_grids).  enable = 0 turns it off. */
+int stkb_set_fused_steps(stkb_domain *dom, int32_t enable);
+
 /* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process
  * per GPU).  Each rank exports its buffers and its 2-slot flag array with CUDA
  * IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and

@@ -243,6 +243,11 @@ class DeviceTarget:
         self._program_key = key
         self._body = body  # keep the id stable
 
+    def set_fused_steps(self, enable: bool) -> None:
+        """Two time steps per sweep for a radius <= 2 Jacobi ping-pong (default on;
+        bit-identical to single steps, include/stkb200.h stkb_set_fused_steps)."""
+        L.call("stkb_set_fused_steps", self.h, int(bool(enable)))
+
     def run(self, steps: int) -> None:
         L.call("stkb_run", self.h, ctypes.c_int64(int(steps)))
         self.total_launches = getattr(self, "total_launches", 0) + self.launches()

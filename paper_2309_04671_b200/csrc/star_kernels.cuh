@@ -47,6 +47,8 @@ struct StarCfg {
     static constexpr int STAGE_ELEMS = HALO_ELEMS + (FORM == FORM_WAVE ? 3 * CTR_ELEMS : 0);
 #ifdef STKB_EXP_NOYHALO
     static constexpr uint32_t HALO_BYTES = SW * BY * sizeof(T);  // experiment: no y-halo rows loaded
+#elif defined(STKB_EXP_NOXHALO)
+    static constexpr uint32_t HALO_BYTES = BX * SH * sizeof(T);  // experiment: no x-halo columns loaded
 #else
     static constexpr uint32_t HALO_BYTES = HALO_ELEMS_RAW * sizeof(T);  // bytes the TMA delivers
 #endif

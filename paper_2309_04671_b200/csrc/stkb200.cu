@@ -43,6 +43,9 @@ struct Star2DArgs {
     int32_t box;
     double cb[81];
 };
+cudaError_t launch_tb2_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
+cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
+int tb2_tile(int dtype, int radius, int* box_w, int* box_h, int* v_w, int* v_h);
 cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
                           cudaStream_t s);
 }  // namespace stkb
@@ -140,6 +143,15 @@ struct stkb_domain {
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
     bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
     int order_y_fast = 0; // STKB_ORDER_Y=1: work items walk y tiles fastest
+    // two time steps per sweep (star_tb.cuh) for the Jacobi ping-pong of a radius <= 2 star:
+    // u(t+2) goes to a scratch buffer bufs[scratch] and u's binding rotates with it
+    bool tb = true;                // STKB_TB=0 disables
+    int scratch = -1;              // index of the scratch buffer in bufs (allocated on first use)
+    bool tb_warmed = false;
+    int64_t ext_writes = 0;        // bumped by every API that hands out or writes buffer memory
+    int64_t tb_pair_epoch = -1;    // ext_writes when bufs[tb_pair[0]] / [1] last had equal frozen parts
+    int tb_pair[2] = {-1, -1};
+    std::map<std::pair<int, int>, cudaGraphExec_t> tb_graphs;  // (u buffer, scratch) -> 2 fused passes
 };
 
 namespace {
@@ -287,6 +299,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     const CUtensorMap* m_halo = nullptr;
 #ifdef STKB_EXP_NOYHALO
     int rc = encode_map(dom, sb, bx + 2 * hx, by, &m_halo);
+#elif defined(STKB_EXP_NOXHALO)
+    int rc = encode_map(dom, sb, bx, by + 2 * R, &m_halo);
 #else
     int rc = encode_map(dom, sb, bx + 2 * hx, by + 2 * R, &m_halo);
 #endif
@@ -380,6 +394,9 @@ int enqueue_step(stkb_domain* dom, std::vector<int32_t>& bind, int64_t* launches
 void invalidate_graph(stkb_domain* dom) {
     for (auto& kv : dom->graphs) cudaGraphExecDestroy(kv.second.first);
     dom->graphs.clear();
+    for (auto& kv : dom->tb_graphs) cudaGraphExecDestroy(kv.second);
+    dom->tb_graphs.clear();
+    dom->tb_warmed = false;
     dom->gperiod = 0;
     dom->warmed = false;
 }
@@ -395,6 +412,76 @@ int binding_period(const stkb_domain* dom) {
         if (cur == b) return k;
     }
     return 0;
+}
+
+// The step program is `v = S(u); swap(u, v)` (either swap order) with S a fast 3-D
+// STAR map of radius <= 2: two steps can run as one fused sweep.  Returns the map.
+const MapOp* tb_map(const stkb_domain* dom) {
+    if (!dom->tb || dom->desc.ndim != 3 || dom->prog.size() != 2) return nullptr;
+    const ProgOp& m = dom->prog[0];
+    const ProgOp& w = dom->prog[1];
+    if (m.kind != 0 || w.kind != 1) return nullptr;
+    const MapOp& op = dom->maps[m.map];
+    const stkb_map_desc& d = op.d;
+    // radius 1 only: at radius 2 the v rows each warp recomputes (TY2 + 4 for TY2 outputs
+    // within the register budget) cost more than the halved HBM traffic saves (measured)
+    if (d.kind != STKB_MAP_STAR || d.radius != 1 || d.precision != STKB_PREC_FAST) return nullptr;
+    if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;
+    if (d.lo[0] >= d.hi[0] || d.lo[1] >= d.hi[1] || d.lo[2] >= d.hi[2]) return nullptr;
+    return &op;
+}
+
+// one fused sweep: u(t+2) = S(S(u(t))) from bufs[binding[u]] into bufs[scratch]; v's buffer
+// supplies the values outside the region box; then u's binding and the scratch swap
+template <typename T>
+int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
+    const stkb_map_desc& d = op.d;
+    const int ub = dom->binding[d.src], vb = dom->binding[d.dst];
+    StarArgs<T> a{};
+    a.g = dom->g;
+    a.box = box_of(d);
+    constexpr int VEC = 16 / sizeof(T);
+    a.x0base = a.box.lo2 - (a.box.lo2 % VEC);
+    a.dst = static_cast<T*>(dom->bufs[dom->scratch]);
+    a.src = static_cast<const T*>(dom->bufs[ub]);
+    a.prev = static_cast<const T*>(dom->bufs[vb]);
+    a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
+    a.work_counter = dom->d_flags + kMaxTags + op.slot;
+    const int R = d.radius;
+    a.c0 = T(d.coef[0]);
+    for (int ax = 0; ax < 3; ++ax)
+        for (int m = 1; m <= 4; ++m) {
+            a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)]) : T(0);
+            a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1]) : T(0);
+        }
+    a.divisor = d.divisor != 0.0 ? T(1.0 / d.divisor) : T(0);
+    int bw, bh, vw, vh;
+    if (tb2_tile(dom->desc.dtype, R, &bw, &bh, &vw, &vh)) return fail(STKB_ERR_UNSUPPORTED, "fused sweep radius");
+    const CUtensorMap *m_halo = nullptr, *m_v = nullptr;
+    if (int rc = encode_map(dom, ub, bw, bh, &m_halo)) return rc;
+    if (int rc = encode_map(dom, vb, vw, vh, &m_v)) return rc;
+    CUtensorMap maps[2] = {*m_halo, *m_v};
+    StarLaunch L{};
+    L.kind = d.kind;
+    L.radius = R;
+    L.has_divisor = d.divisor != 0.0;
+    L.maps = maps;
+    L.box_w = bw;
+    L.box_h = bh;
+    L.num_sms = dom->num_sms;
+    L.max_ctas = dom->ctas_override;
+    L.lz = dom->lz_override;
+    L.taper = dom->taper;
+    cudaError_t e;
+    if constexpr (sizeof(T) == 4) e = launch_tb2_f32(L, a, dom->stream);
+    else e = launch_tb2_f64(L, a, dom->stream);
+    if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("fused star kernel launch: ") + cudaGetErrorString(e));
+    std::swap(dom->binding[d.src], dom->scratch);
+    return STKB_OK;
+}
+
+int enqueue_tb2(stkb_domain* dom, const MapOp& op) {
+    return dom->desc.dtype == STKB_F32 ? launch_tb2_map<float>(dom, op) : launch_tb2_map<double>(dom, op);
 }
 
 int check_name(const stkb_domain* dom, int32_t n, const char* what) {
@@ -477,6 +564,7 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_STORE_HINT")) dom->store_hint = atoi(s);
     if (const char* s = getenv("STKB_TAPER")) dom->taper = atoi(s) != 0;
     if (const char* s = getenv("STKB_ORDER_Y")) dom->order_y_fast = atoi(s);
+    if (const char* s = getenv("STKB_TB")) dom->tb = atoi(s) != 0;
     *out = dom;
     return STKB_OK;
 }
@@ -515,6 +603,7 @@ int stkb_layout(const stkb_domain* dom, int64_t* pitch, int64_t* plane, int64_t*
 int stkb_device_ptr(stkb_domain* dom, int32_t name, void** dptr) {
     if (!dom || !dptr) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_device_ptr")) return rc;
+    ++dom->ext_writes;  // the caller may write through the pointer
     *dptr = dom->bufs[dom->binding[name]];
     return STKB_OK;
 }
@@ -524,6 +613,7 @@ int stkb_zero(stkb_domain* dom, int32_t name) {
     if (int rc = check_name(dom, name, "stkb_zero")) return rc;
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
+    ++dom->ext_writes;
     CUDA_TRY(cudaMemsetAsync(dom->bufs[dom->binding[name]], 0, bytes, dom->stream));
     return STKB_OK;
 }
@@ -549,6 +639,7 @@ static bool ensure_stage(stkb_domain* dom, size_t want) {
 }
 
 static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
+    ++dom->ext_writes;
     if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_upload")) return rc;
     CUDA_TRY(cudaSetDevice(dom->desc.device));
@@ -758,15 +849,100 @@ int stkb_program_add_swap(stkb_domain* dom, int32_t a, int32_t b) {
     return STKB_OK;
 }
 
+// CUDA graph of two fused sweeps from the current (u buffer, scratch) pair; capturing
+// runs nothing
+int tb_graph(stkb_domain* dom, const MapOp& tb, cudaGraphExec_t* out) {
+    const std::pair<int, int> key(dom->binding[tb.d.src], dom->scratch);
+    auto it = dom->tb_graphs.find(key);
+    if (it == dom->tb_graphs.end()) {
+        CUDA_TRY(cudaStreamBeginCapture(dom->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_tb2(dom, tb);
+        if (rc == STKB_OK) rc = enqueue_tb2(dom, tb);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(dom->stream, &graph);
+        dom->binding[tb.d.src] = key.first;  // capturing did not run the sweeps
+        dom->scratch = key.second;
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ex = nullptr;
+        e = cudaGraphInstantiate(&ex, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        it = dom->tb_graphs.emplace(key, ex).first;
+    }
+    *out = it->second;
+    return STKB_OK;
+}
+
 int stkb_run(stkb_domain* dom, int64_t steps) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     if (steps < 0) return fail(STKB_ERR_ARG, "negative step count");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
-    CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
     int64_t launches = 0;
     int64_t done = 0;
     const int period = binding_period(dom);
     const bool graphs_ok = period > 0 && getenv("STKB_NO_GRAPH") == nullptr;
+    if (const MapOp* tb = steps >= 4 ? tb_map(dom) : nullptr) {
+        // fused sweeps for all but the last 2..3 steps, which run as single steps so
+        // that v ends up holding its own final value
+        const int64_t n_tb = (steps - 2) / 2;
+        const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
+        if (dom->scratch < 0) {  // host-side setup stays outside the timed events
+            void* b = nullptr;
+            CUDA_TRY(cudaMalloc(&b, bytes));
+            dom->bufs.push_back(b);
+            dom->scratch = int(dom->bufs.size()) - 1;
+            dom->tb_pair_epoch = -1;
+        }
+        cudaGraphExec_t gx = nullptr;
+        if (graphs_ok && dom->tb_warmed && n_tb >= 2)
+            if (int rc = tb_graph(dom, *tb, &gx)) return rc;
+        CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
+        // the scratch takes over u's halo and whatever interior the region leaves alone
+        // (the fused kernel writes only the region); skipped while both still match
+        const int ub = dom->binding[tb->d.src];
+        const bool paired = dom->tb_pair_epoch == dom->ext_writes &&
+                            ((dom->tb_pair[0] == ub && dom->tb_pair[1] == dom->scratch) ||
+                             (dom->tb_pair[1] == ub && dom->tb_pair[0] == dom->scratch));
+        if (!paired) {
+            CUDA_TRY(cudaMemcpyAsync(dom->bufs[dom->scratch], dom->bufs[ub], bytes, cudaMemcpyDeviceToDevice,
+                                     dom->stream));
+            dom->tb_pair[0] = ub;
+            dom->tb_pair[1] = dom->scratch;
+            dom->tb_pair_epoch = dom->ext_writes;
+        }
+        int64_t k = 0;
+        if (!dom->tb_warmed || !graphs_ok) {  // attributes and tensor maps outside any capture
+            if (int rc = enqueue_tb2(dom, *tb)) return rc;
+            ++launches;
+            dom->tb_warmed = true;
+            k = 1;
+        }
+        if (graphs_ok && n_tb - k >= 2) {
+            if (k > 0)  // after the warm-up sweep (captured while it runs)
+                if (int rc = tb_graph(dom, *tb, &gx)) return rc;
+            const int64_t reps = (n_tb - k) / 2;
+            for (int64_t r = 0; r < reps; ++r) CUDA_TRY(cudaGraphLaunch(gx, dom->stream));
+            launches += 2 * reps;
+            k += 2 * reps;  // two rotations: u and the scratch are back where they started
+        }
+        for (; k < n_tb; ++k) {
+            if (int rc = enqueue_tb2(dom, *tb)) return rc;
+            ++launches;
+        }
+        // the binding of 2 n_tb single steps (a ping-pong swap twice per pair: unchanged)
+        done = 2 * n_tb;
+        for (; done < steps; ++done)
+            if (int rc = enqueue_step(dom, dom->binding, &launches)) return rc;
+        CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
+        dom->timed = true;
+        dom->last_launches = launches;
+        return STKB_OK;
+    }
+    CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
     // the first step after a program change runs uncaptured: it sets kernel
     // attributes and encodes tensor maps outside any capture
     if (graphs_ok && !dom->warmed && steps > 0) {
@@ -944,6 +1120,7 @@ int stkb_peer_fetch_halo(stkb_domain* dom, void* stream, int32_t planes) {
     if (planes < 0 || planes > dom->g.order0) return fail(STKB_ERR_ARG, "planes must be in 0..order");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dom->stream;
+    ++dom->ext_writes;
     const size_t pb = size_t(dom->g.plane) * dom->elem;
     for (int side = 0; side < 2; ++side) {
         const auto& p = dom->peer[side];
@@ -1091,6 +1268,12 @@ int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, i
     return STKB_OK;
 }
 
+int stkb_set_fused_steps(stkb_domain* dom, int32_t enable) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->tb = enable != 0;
+    return STKB_OK;
+}
+
 int stkb_set_max_ctas(stkb_domain* dom, int32_t ctas) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     dom->ctas_override = std::max<int32_t>(0, ctas);
@@ -1108,6 +1291,7 @@ int stkb_apply_swap(stkb_domain* dom, int32_t a, int32_t b) {
 int stkb_plane_span(stkb_domain* dom, int32_t name, int64_t z0, int64_t nplanes, void** dptr, int64_t* bytes) {
     if (!dom || !dptr || !bytes) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_plane_span")) return rc;
+    ++dom->ext_writes;
     const Geometry& g = dom->g;
     if (nplanes < 0 || z0 < -g.order0 || z0 + nplanes > g.n0 + g.order0)
         return fail(STKB_ERR_ARG, "plane span outside the padded grid");

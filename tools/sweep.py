@@ -27,7 +27,8 @@ def time_one(builder, shape, dtype, steps=20, warm=3):
     bench.fill_device(dt, names, shape, builder)
     dt.set_program(body)
     dt.run(warm)
-    dt.run(2)
+    dt.run(steps)  # graphs and fused-sweep scratch for the timed run's start state
+    dt.run(steps)
     dt.sync()
     dt.run(steps)
     dt.sync()

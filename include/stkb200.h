@@ -175,7 +175,9 @@ int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (le
  * the last 2..3 steps singly, so every grid ends with exactly the single-step
  * kernel's values (bit for bit; the fused sweep keeps each step's FMA order).  It
  * allocates one scratch grid; u's name rotates between its buffer and the scratch
- * (stkb_binding may then report buffer index n_grids).  enable = 0 turns it off. */
+ * (stkb_binding may then report buffer index n_grids).  Such a run also launches one
+ * small check kernel (are v's frozen values next to the region all zero? then the
+ * sweeps need not stage them): stkb_launches counts it.  enable = 0 turns it off. */
 int stkb_set_fused_steps(stkb_domain *dom, int32_t enable);
 
 /* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process

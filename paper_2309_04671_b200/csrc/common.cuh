@@ -61,6 +61,7 @@ struct StarArgs {
     // when bit 1 is — over NVLink, in place of this slab's own halo planes
     int32_t pull;
     int32_t pull_lo_n0;
+    const int32_t* frozen_nz;  // fused sweeps: != 0 when v's frozen values next to the box are not all zero
     T cb[729];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 4 (last: the
                                // other fields keep their parameter-bank offsets)
 };

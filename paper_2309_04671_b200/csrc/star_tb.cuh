@@ -88,6 +88,8 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
         if (lane == 0) {
             prefetch_tmap(&tm_src);
             prefetch_tmap(&tm_v);
+            // v's frozen values around the box are all zero (the usual zero halo): no v tiles
+            const bool need_v = *reinterpret_cast<const volatile int32_t*>(a.frozen_nz) != 0;
             uint32_t it = 0;
             while (true) {
                 const int item = atomicAdd(a.work_counter, 1);
@@ -114,7 +116,8 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                     mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
                     stage_item[s] = item;
                     const int qv = q - R;  // v plane completed with this stage
-                    const bool vload = qv >= z0 - R && qv < z1 + R && (edge_xy || qv < a.box.lo0 || qv >= a.box.hi0);
+                    const bool vload = need_v && qv >= z0 - R && qv < z1 + R &&
+                                       (edge_xy || qv < a.box.lo0 || qv >= a.box.hi0);
                     T* st = tiles + size_t(s) * C::STAGE_ELEMS;
                     mbar_arrive_expect_tx(&full[s], C::HALO_BYTES + (vload ? C::V_BYTES : 0u));
                     // planes beyond the allocation (q < -order0 or q >= n0 + order0) are
@@ -153,6 +156,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     T chk1 = T(0);
     uint32_t it = 0;
     const int64_t pitch = a.g.pitch, plane = a.g.plane;
+    const bool need_v = *reinterpret_cast<const volatile int32_t*>(a.frozen_nz) != 0;
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
@@ -302,8 +306,8 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                             for (int j = 0; j < TY1; ++j) {
                                 const int y = yv + j;
                                 const bool row_in = z_in && y >= a.box.lo1 && y < a.box.hi1;
-                                T fz[VEC];
-                                lds16(vt + j * C::VW, fz);
+                                T fz[VEC] = {};
+                                if (need_v) lds16(vt + j * C::VW, fz);
 #pragma unroll
                                 for (int e = 0; e < VEC; ++e) {
                                     const int xx = xv + e;
@@ -456,6 +460,41 @@ struct TbTile {
     static constexpr int TY2 = CODE / 100;
     static constexpr int NW = CODE % 100;
 };
+
+// *flag |= 1 when a cell of `buf` within R of the box (along any axis, outside it) is not
+// bit-for-bit +0: the fused sweep then stages v's frozen values through TMA
+template <typename T>
+__global__ void frozen_ring_kernel(const T* __restrict__ buf, Geometry g, Box b, int R, int32_t* flag) {
+    const int64_t X = int64_t(b.hi2 - b.lo2) + 2 * R, Y = int64_t(b.hi1 - b.lo1) + 2 * R;
+    const int64_t nz = int64_t(b.hi0 - b.lo0), ny = int64_t(b.hi1 - b.lo1), nx = int64_t(b.hi2 - b.lo2);
+    const int64_t nA = 2 * R * Y * X, nB = nz * 2 * R * X, nC = nz * ny * 2 * R;
+    bool nonzero = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nA + nB + nC;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t z, y, x;
+        if (i < nA) {  // planes below / above the box
+            const int64_t k = i / (Y * X), r = i - k * Y * X;
+            z = k < R ? b.lo0 - R + k : b.hi0 + (k - R);
+            y = b.lo1 - R + r / X;
+            x = b.lo2 - R + r % X;
+        } else if (i < nA + nB) {  // rows before / after, inside the box's planes
+            const int64_t j = i - nA, zz = j / (2 * R * X), r = j - zz * 2 * R * X, k = r / X;
+            z = b.lo0 + zz;
+            y = k < R ? b.lo1 - R + k : b.hi1 + (k - R);
+            x = b.lo2 - R + r % X;
+        } else {  // columns left / right, inside the box's rows
+            const int64_t j = i - nA - nB, row = j / (2 * R), k = j - row * 2 * R;
+            z = b.lo0 + row / ny;
+            y = b.lo1 + row % ny;
+            x = k < R ? b.lo2 - R + k : b.hi2 + (k - R);
+        }
+        const T v = buf[g.at(z, y, x)];
+        if constexpr (sizeof(T) == 4) nonzero |= __float_as_uint(v) != 0u;
+        else nonzero |= __double_as_longlong(v) != 0ll;
+    }
+    (void)nx;
+    if (__any_sync(0xffffffffu, nonzero) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
 
 template <typename T, int R, bool DIV>
 cudaError_t launch_tb2_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* map, cudaStream_t stream) {

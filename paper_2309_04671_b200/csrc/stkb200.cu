@@ -46,6 +46,8 @@ struct Star2DArgs {
 cudaError_t launch_tb2_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
 cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
 int tb2_tile(int dtype, int radius, int* box_w, int* box_h, int* v_w, int* v_h);
+cudaError_t launch_frozen_ring(int dtype, const Geometry& g, const Box& b, int R, const void* buf, int32_t* flag,
+                               int num_sms, cudaStream_t s);
 cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
                           cudaStream_t s);
 }  // namespace stkb
@@ -70,6 +72,8 @@ int fail(int code, const std::string& msg) {
 
 constexpr int kMaxTags = 64;
 constexpr int kMaxMaps = 256;
+constexpr int kFrozenFlag = kMaxTags + 2 * kMaxMaps;  // d_flags slot: v's frozen ring is not all zero
+constexpr int kNumFlags = kFrozenFlag + 4;
 
 struct MapOp {
     stkb_map_desc d;
@@ -447,6 +451,7 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     a.prev = static_cast<const T*>(dom->bufs[vb]);
     a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
     a.work_counter = dom->d_flags + kMaxTags + op.slot;
+    a.frozen_nz = dom->d_flags + kFrozenFlag;
     const int R = d.radius;
     a.c0 = T(d.coef[0]);
     for (int ax = 0; ax < 3; ++ax)
@@ -551,8 +556,8 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (cudaEventCreate(&dom->ev0) != cudaSuccess || cudaEventCreate(&dom->ev1) != cudaSuccess) return cleanup("event");
     // [0, kMaxTags): sticky non-finite flags per map tag; then one scheduler counter
     // per map; then one boundary-signal counter per map (slab halo exchange)
-    if (cudaMalloc(&dom->d_flags, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
-    cudaMemset(dom->d_flags, 0, (kMaxTags + 2 * kMaxMaps) * sizeof(int32_t));
+    if (cudaMalloc(&dom->d_flags, kNumFlags * sizeof(int32_t)) != cudaSuccess) return cleanup("flags");
+    cudaMemset(dom->d_flags, 0, kNumFlags * sizeof(int32_t));
     if (cudaMalloc(&dom->d_peer_flags, 2 * sizeof(int32_t)) != cudaSuccess) return cleanup("peer flags");
     {
         const int32_t done0[2] = {peer_mask(0), peer_mask(0)};  // "launch 0 completed"
@@ -914,6 +919,11 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
             dom->tb_pair[1] = dom->scratch;
             dom->tb_pair_epoch = dom->ext_writes;
         }
+        // are v's values next to the box (its halo, for a full-interior map) all zero?
+        CUDA_TRY(launch_frozen_ring(dom->desc.dtype, dom->g, box_of(tb->d), tb->d.radius,
+                                    dom->bufs[dom->binding[tb->d.dst]], dom->d_flags + kFrozenFlag, dom->num_sms,
+                                    dom->stream));
+        ++launches;
         int64_t k = 0;
         if (!dom->tb_warmed || !graphs_ok) {  // attributes and tensor maps outside any capture
             if (int rc = enqueue_tb2(dom, *tb)) return rc;

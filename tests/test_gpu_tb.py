@@ -58,7 +58,7 @@ def _fused_launches(steps, builder="star3d1r"):
     if "1r" not in builder and builder != "jacobi7":
         return steps  # radius 2+: single steps (stkb200.cu tb_map)
     n_tb = (steps - 2) // 2
-    return n_tb + steps - 2 * n_tb
+    return n_tb + steps - 2 * n_tb + 1  # + the frozen-ring check kernel
 
 
 @pytest.mark.parametrize("builder,dtype", [("star3d1r", "f32"), ("jacobi7", "f32"), ("star3d1r_norm", "f32"),
@@ -86,6 +86,23 @@ def test_fused_sweeps_sub_box_and_halo_bitwise(builder, dtype, box):
     assert n2 == _fused_launches(steps)
     for n in one:
         assert np.array_equal(one[n], two[n]), (builder, dtype, box, n)
+
+
+@pytest.mark.parametrize("halo", [0.0, -0.0, 1e-30])
+def test_fused_sweeps_zero_and_nonzero_halo_bitwise(halo):
+    """Zero halo: the sweeps skip staging v's frozen values (ring check); -0.0 and a tiny
+    non-zero halo must take the staged path and still match single steps bit for bit."""
+    steps = 8
+    bound, grids = _inputs("star3d1r", (33, 70, 250), "f32", steps)
+    for n in ("u", "v"):
+        g = grids[n]
+        inner = g.interior.copy()
+        g.data[...] = halo
+        g.interior[...] = inner
+    one, _ = _device_run(bound, grids, steps, fused=False)
+    two, _ = _device_run(bound, grids, steps, fused=True)
+    for n in one:
+        assert np.array_equal(one[n].view(np.uint32), two[n].view(np.uint32)), (halo, n)
 
 
 @pytest.mark.parametrize("builder,dtype,shape", [("jacobi7", "f32", (96, 80, 200)), ("star3d1r", "f64", (33, 40, 70)),

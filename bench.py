@@ -194,6 +194,20 @@ def run_ours(args) -> None:
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    if ws > 1 and args.watchdog > 0:
+        # a rank that never returns (e.g. a neighbour died and its step flag never comes)
+        # ends the run with an error line instead of hanging the job
+        import threading
+
+        def _expire():
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "n_gpus": ws,
+                                  "error": f"watchdog: no result after {args.watchdog} s"}), flush=True)
+            os._exit(3)
+
+        wd = threading.Timer(args.watchdog, _expire)
+        wd.daemon = True
+        wd.start()
     if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
@@ -408,6 +422,8 @@ def main() -> None:
     ap.add_argument("--force-slabs", action="store_true",
                     help="use the z-slab/NCCL engine even on one GPU (tests the multi-GPU path)")
     ap.add_argument("--shape", default=None, help=argparse.SUPPRESS)  # tests: smaller grid of the config
+    ap.add_argument("--watchdog", type=float, default=1200.0,
+                    help="N>1: seconds after which a run that has not finished exits with an error line")
     ap.add_argument("--traffic", type=float, default=None,
                     help="DRAM bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()

@@ -180,6 +180,11 @@ int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (le
  * sweeps need not stage them): stkb_launches counts it.  enable = 0 turns it off. */
 int stkb_set_fused_steps(stkb_domain *dom, int32_t enable);
 
+/* Let `device` read and write `peer`'s memory (cudaDeviceEnablePeerAccess; already
+ * enabled is fine).  Used to wire in-process slab domains on different GPUs
+ * (slabs.connect_local, the peer-pull probe); IPC-opened memory does not need it. */
+int stkb_enable_peer(int32_t device, int32_t peer);
+
 /* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process
  * per GPU).  Each rank exports its buffers and its 2-slot flag array with CUDA
  * IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and

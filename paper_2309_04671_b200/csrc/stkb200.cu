@@ -1278,6 +1278,21 @@ int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, i
     return STKB_OK;
 }
 
+int stkb_enable_peer(int32_t device, int32_t peer) {
+    if (device == peer) return STKB_OK;
+    int ok = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&ok, device, peer));
+    if (!ok) return fail(STKB_ERR_UNSUPPORTED, "no peer access between these GPUs");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();  // clear the non-sticky error
+        e = cudaSuccess;
+    }
+    CUDA_TRY(e);
+    return STKB_OK;
+}
+
 int stkb_set_fused_steps(stkb_domain* dom, int32_t enable) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     dom->tb = enable != 0;

@@ -312,6 +312,12 @@ class DeviceSlabEngine:
     def _device_uuid(self, ordinal: int) -> str:
         return str(getattr(self.torch.cuda.get_device_properties(ordinal), "uuid", ordinal))
 
+    def _device_of(self, uuid: str) -> Optional[int]:
+        for d in range(self.torch.cuda.device_count()):
+            if self._device_uuid(d) == uuid:
+                return d
+        return None
+
     def _can_reach(self, uuid: str) -> bool:
         """Can this GPU read memory on the GPU with this uuid (same device, or peer access)?"""
         me = self.dt.device
@@ -487,6 +493,16 @@ class DeviceSlabEngine:
         dist.all_gather_object(every, mine)
         ok = all(self._can_reach(every[p]["uuid"]) for p in (self.plan.lower, self.plan.upper) if p is not None)
         why = "z-slab neighbours without peer access"
+        if ok and self.plan.rank == 0 and self.plan.upper is not None:
+            # TMA loads from another GPU's memory: proven in a child process first
+            # (peer_probe.py); a fault there must not take this run down
+            import os
+
+            peer = self._device_of(every[self.plan.upper]["uuid"])
+            if peer is not None and peer != self.dt.device and os.environ.get("STKB_PEER_PROBE", "1") != "0":
+                from .peer_probe import probe
+
+                ok, why = probe(self.dt.device, peer)
         if ok:
             try:
                 for side, peer in ((0, self.plan.lower), (1, self.plan.upper)):
@@ -556,6 +572,7 @@ def connect_local(engines: list) -> None:
     for i, e in enumerate(engines):
         for side, j in ((0, i - 1), (1, i + 1)):
             if 0 <= j < len(engines):
+                L.call("stkb_enable_peer", e.dt.device, engines[j].dt.device)
                 bufs, flags = ptrs(engines[j])
                 arr = (ctypes.c_void_p * len(bufs))(*bufs)
                 L.call("stkb_set_peer", e.dt.h, side, len(bufs), arr, ctypes.c_void_p(flags),

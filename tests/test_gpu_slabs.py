@@ -270,3 +270,14 @@ def test_p2p_graph_replay_matches_unsplit_oracle(world, builder, shape, steps):
         assert rep.max_relative <= 1e-5, (n, rep.render())
     for eng in engines:
         eng.close()
+
+
+def test_peer_pull_probe_on_one_device():
+    """The multi-GPU transport probe (peer_probe.py) run with both slabs on cuda:0: the
+    2-slab fused-exchange result is bit-identical to the unsplit run, in-process and
+    through the child process the multi-GPU runs use."""
+    from paper_2309_04671_b200 import peer_probe
+
+    assert peer_probe.run(0, 0)["ok"]
+    ok, why = peer_probe.probe(0, 0)
+    assert ok, why

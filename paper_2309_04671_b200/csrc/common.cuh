@@ -61,7 +61,6 @@ struct StarArgs {
     // when bit 1 is — over NVLink, in place of this slab's own halo planes
     int32_t pull;
     int32_t pull_lo_n0;
-    const int32_t* frozen_nz;  // fused sweeps: != 0 when v's frozen values next to the box are not all zero
     T cb[729];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 4 (last: the
                                // other fields keep their parameter-bank offsets)
 };
@@ -189,6 +188,7 @@ struct StarLaunch {
     int n_signal_ranges;   // the first ranges are "signal" ranges (one chunk each)
     int32_t* signal;       // counter bumped once per stored signal item
     int* signal_items;     // out: number of signal items of this launch
+    const int32_t* frozen_nz;  // fused sweeps: != 0 when v's frozen values next to the box are not all zero
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);

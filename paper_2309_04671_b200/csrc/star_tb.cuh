@@ -56,7 +56,7 @@ struct TbCfg {
 template <typename T, int R, int TY2, int NW, bool DIV>
 __global__ void __launch_bounds__((NW + 1) * 32, 1)
 star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_v,
-                const __grid_constant__ StarArgs<T> a) {
+                const __grid_constant__ StarArgs<T> a, const int32_t* __restrict__ frozen_nz) {
     using C = TbCfg<T, R, TY2, NW>;
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, TY1 = C::TY1;
     constexpr int STAGES = C::STAGES;
@@ -89,7 +89,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
             prefetch_tmap(&tm_src);
             prefetch_tmap(&tm_v);
             // v's frozen values around the box are all zero (the usual zero halo): no v tiles
-            const bool need_v = *reinterpret_cast<const volatile int32_t*>(a.frozen_nz) != 0;
+            const bool need_v = *reinterpret_cast<const volatile int32_t*>(frozen_nz) != 0;
             uint32_t it = 0;
             while (true) {
                 const int item = atomicAdd(a.work_counter, 1);
@@ -156,7 +156,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     T chk1 = T(0);
     uint32_t it = 0;
     const int64_t pitch = a.g.pitch, plane = a.g.plane;
-    const bool need_v = *reinterpret_cast<const volatile int32_t*>(a.frozen_nz) != 0;
+    const bool need_v = *reinterpret_cast<const volatile int32_t*>(frozen_nz) != 0;
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
@@ -528,7 +528,7 @@ cudaError_t launch_tb2_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap
     const int grid = a.n_items < ctas ? a.n_items : ctas;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(map[0], map[1], a);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(map[0], map[1], a, L.frozen_nz);
     return cudaGetLastError();
 }
 

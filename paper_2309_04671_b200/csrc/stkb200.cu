@@ -451,7 +451,6 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     a.prev = static_cast<const T*>(dom->bufs[vb]);
     a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
     a.work_counter = dom->d_flags + kMaxTags + op.slot;
-    a.frozen_nz = dom->d_flags + kFrozenFlag;
     const int R = d.radius;
     a.c0 = T(d.coef[0]);
     for (int ax = 0; ax < 3; ++ax)
@@ -471,6 +470,7 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     L.radius = R;
     L.has_divisor = d.divisor != 0.0;
     L.maps = maps;
+    L.frozen_nz = dom->d_flags + kFrozenFlag;
     L.box_w = bw;
     L.box_h = bh;
     L.num_sms = dom->num_sms;

@@ -46,7 +46,8 @@ struct TbCfg {
     static constexpr uint32_t V_BYTES = VW * VH * sizeof(T);
     static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * sizeof(T);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+    // a power of two: the stage index and phase of plane `it` are a mask and a shift
+    static constexpr int STAGES = STAGES_RAW >= 8 ? 8 : (STAGES_RAW >= 4 ? 4 : 2);
     static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
                                    STAGES * sizeof(int32_t);
     static constexpr int THREADS = (NW + 1) * 32;

@@ -1,9 +1,10 @@
 // Two time steps per d0 sweep (temporal blocking) for the Jacobi ping-pong
-// `v = S(u); swap(u, v)` with a star S of radius R <= 2.
+// `v = S(u); swap(u, v)` with a star S of radius R (written for R <= VEC; built and
+// routed for R = 1, where it wins: DESIGN.md §3.1b).
 //
 // The single-step kernel (star_kernels.cuh) moves 8 B (fp32) per point and step
-// through HBM; for radius 1..2 the arithmetic and shared-memory work per point
-// are small, so the step is HBM-bound.  This kernel streams u once and produces
+// through HBM; at radius 1 the arithmetic and shared-memory work per point are
+// small, so the step is HBM-bound.  This kernel streams u once and produces
 // u(t+2) = S(S(u(t))): every plane of v(t+1) is computed in registers and
 // consumed in registers, halving the HBM bytes per step.  Same semantics and the
 // same per-step arithmetic (identical FMA order) as two launches of the
@@ -440,24 +441,18 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     if (__any_sync(0xffffffffu, !K::clean(chk) || chk1 != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
-// tile of the fused kernel per dtype and radius, coded 100 * (output rows per warp) +
-// consumer warps: the largest that keeps both register rings spill-free (ptxas -v)
+// tile of the fused kernel per dtype (radius 1), coded 100 * (output rows per warp) +
+// consumer warps: measured best of 2..5 rows x 7..12 warps, spill-free (ptxas -v)
 #ifndef STKB_TB_F32R1
 #define STKB_TB_F32R1 311
-#endif
-#ifndef STKB_TB_F32R2
-#define STKB_TB_F32R2 207
 #endif
 #ifndef STKB_TB_F64R1
 #define STKB_TB_F64R1 311
 #endif
-#ifndef STKB_TB_F64R2
-#define STKB_TB_F64R2 207
-#endif
 template <typename T, int R>
 struct TbTile {
-    static constexpr int CODE = sizeof(T) == 4 ? (R == 1 ? STKB_TB_F32R1 : STKB_TB_F32R2)
-                                               : (R == 1 ? STKB_TB_F64R1 : STKB_TB_F64R2);
+    static_assert(R == 1, "fused sweeps are tuned and routed for radius 1 (stkb200.cu tb_map)");
+    static constexpr int CODE = sizeof(T) == 4 ? STKB_TB_F32R1 : STKB_TB_F64R1;
     static constexpr int TY2 = CODE / 100;
     static constexpr int NW = CODE % 100;
 };
@@ -542,15 +537,9 @@ cudaError_t launch_tb2_r(const StarLaunch& L, const StarArgs<T>& a, cudaStream_t
 // host: the TMA boxes of the fused tile (u with its 2R halo; the frozen v tile)
 template <typename T>
 inline int tb2_tile_t(int R, int* box_w, int* box_h, int* v_w, int* v_h) {
-    if (R == 1) {
-        using C = TbCfg<T, 1, TbTile<T, 1>::TY2, TbTile<T, 1>::NW>;
-        *box_w = C::SW; *box_h = C::SH; *v_w = C::VW; *v_h = C::VH;
-    } else if (R == 2) {
-        using C = TbCfg<T, 2, TbTile<T, 2>::TY2, TbTile<T, 2>::NW>;
-        *box_w = C::SW; *box_h = C::SH; *v_w = C::VW; *v_h = C::VH;
-    } else {
-        return 1;
-    }
+    if (R != 1) return 1;
+    using C = TbCfg<T, 1, TbTile<T, 1>::TY2, TbTile<T, 1>::NW>;
+    *box_w = C::SW; *box_h = C::SH; *v_w = C::VW; *v_h = C::VH;
     return 0;
 }
 

@@ -48,6 +48,7 @@ cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaS
 int tb2_tile(int dtype, int radius, int* box_w, int* box_h, int* v_w, int* v_h);
 cudaError_t launch_frozen_ring(int dtype, const Geometry& g, const Box& b, int R, const void* buf, int32_t* flag,
                                int num_sms, cudaStream_t s);
+cudaError_t launch_copy_halo(const void* src, void* dst, const Geometry& g, int esz, int num_sms, cudaStream_t s);
 cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
                           cudaStream_t s);
 }  // namespace stkb
@@ -900,6 +901,8 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
             CUDA_TRY(cudaMalloc(&b, bytes));
             dom->bufs.push_back(b);
             dom->scratch = int(dom->bufs.size()) - 1;
+            // zero pitch padding, as in every grid buffer (kernels never write it)
+            CUDA_TRY(cudaMemsetAsync(b, 0, bytes, dom->stream));
             dom->tb_pair_epoch = -1;
         }
         cudaGraphExec_t gx = nullptr;
@@ -913,8 +916,17 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
                             ((dom->tb_pair[0] == ub && dom->tb_pair[1] == dom->scratch) ||
                              (dom->tb_pair[1] == ub && dom->tb_pair[0] == dom->scratch));
         if (!paired) {
-            CUDA_TRY(cudaMemcpyAsync(dom->bufs[dom->scratch], dom->bufs[ub], bytes, cudaMemcpyDeviceToDevice,
-                                     dom->stream));
+            const stkb_map_desc& d = tb->d;
+            const bool whole = d.lo[0] == 0 && d.lo[1] == 0 && d.lo[2] == 0 && d.hi[0] == dom->g.n0 &&
+                               d.hi[1] == dom->g.n1 && d.hi[2] == dom->g.n2;
+            if (whole) {  // only the halo shell is u's own: the sweeps write the whole interior
+                CUDA_TRY(launch_copy_halo(dom->bufs[ub], dom->bufs[dom->scratch], dom->g, int(dom->elem),
+                                          dom->num_sms, dom->stream));
+                ++launches;
+            } else {
+                CUDA_TRY(cudaMemcpyAsync(dom->bufs[dom->scratch], dom->bufs[ub], bytes, cudaMemcpyDeviceToDevice,
+                                         dom->stream));
+            }
             dom->tb_pair[0] = ub;
             dom->tb_pair[1] = dom->scratch;
             dom->tb_pair_epoch = dom->ext_writes;

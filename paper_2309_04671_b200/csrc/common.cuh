@@ -55,6 +55,8 @@ struct StarArgs {
     T wave_a, wave_b;
     int32_t store_hint;        // 1: streaming (evict-first) output stores
     int32_t order_y_fast;      // work items walk y tiles fastest
+    int32_t band_rows;         // > 0: items walk bands of this many tile rows, every chunk of a band
+                               // before the next band (a band is about one wave of CTAs)
     // fused halo exchange (multi-GPU z-slabs): src planes q < 0 are read by TMA
     // straight from the lower neighbour's buffer (its plane pull_lo_n0 + q) when
     // bit 0 of `pull` is set, planes q >= n0 from the upper neighbour's (plane q - n0)
@@ -189,6 +191,7 @@ struct StarLaunch {
     int32_t* signal;       // counter bumped once per stored signal item
     int* signal_items;     // out: number of signal items of this launch
     const int32_t* frozen_nz;  // fused sweeps: != 0 when v's frozen values next to the box are not all zero
+    int band_pct = 0;      // item order: tile-row bands of band_pct % of a wave (0 = z-major)
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);

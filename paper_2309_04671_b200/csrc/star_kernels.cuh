@@ -123,6 +123,21 @@ template <> struct Pk<double> {
 // neighbours.  order_y_fast walks y tiles fastest (experiment switch).
 template <typename A>
 __device__ __forceinline__ void decode_item(const A& a, int item, int& tx, int& ty, int& tz) {
+    if (a.band_rows > 0) {
+        // bands of about one wave of tiles, each band's chunks in order: chunk k+1 of a
+        // tile is handed out while chunk k still runs, so the 2R planes both read are
+        // one DRAM read; y-neighbours inside a band stay n_tx items apart
+        const int per_band = a.band_rows * a.n_tx * a.n_tz;
+        const int band = item / per_band;
+        const int rem = item - band * per_band;
+        const int rows = min(a.band_rows, a.n_ty - band * a.band_rows);
+        const int tiles = rows * a.n_tx;
+        tz = rem / tiles;
+        const int r = rem - tz * tiles;
+        ty = band * a.band_rows + r / a.n_tx;
+        tx = r - (r / a.n_tx) * a.n_tx;
+        return;
+    }
     const int per = a.n_tx * a.n_ty;
     tz = item / per;
     const int r = item - tz * per;
@@ -643,6 +658,12 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
         k = chunk_range(rlo[i], rhi[i] - rlo[i], a.lz, tiles, ctas, L.taper, a.zs, k);
     a.n_tz = k;
     a.n_signal = nsig;
+    // bands of ~one wave (STKB_BAND = wave fraction in %, 0 = plain z-major order)
+    a.band_rows = 0;
+    if (nsig == 0 && L.band_pct > 0 && a.n_tx > 0) {
+        const int rows = std::max(1, (ctas * L.band_pct / 100) / a.n_tx);
+        if (rows < a.n_ty) a.band_rows = rows;
+    }
     a.signal = L.signal;
     if (L.signal_items) *L.signal_items = tiles * nsig;
     a.n_items = tiles * a.n_tz;

@@ -148,6 +148,7 @@ struct stkb_domain {
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
     bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
     int order_y_fast = 0; // STKB_ORDER_Y=1: work items walk y tiles fastest
+    int band_pct = 100;   // STKB_BAND: item order in tile-row bands of this % of a wave (0: z-major; StarArgs::band_rows)
     // two time steps per sweep (star_tb.cuh) for the Jacobi ping-pong of a radius <= 2 star:
     // u(t+2) goes to a scratch buffer bufs[scratch] and u's binding rotates with it
     bool tb = true;                // STKB_TB=0 disables
@@ -343,6 +344,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;
     L.taper = dom->taper;
+    L.band_pct = dom->band_pct;
     L.n_ranges = rs.n;
     L.rlo = rs.lo;
     L.rhi = rs.hi;
@@ -570,6 +572,7 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_STORE_HINT")) dom->store_hint = atoi(s);
     if (const char* s = getenv("STKB_TAPER")) dom->taper = atoi(s) != 0;
     if (const char* s = getenv("STKB_ORDER_Y")) dom->order_y_fast = atoi(s);
+    if (const char* s = getenv("STKB_BAND")) dom->band_pct = atoi(s);
     if (const char* s = getenv("STKB_TB")) dom->tb = atoi(s) != 0;
     *out = dom;
     return STKB_OK;

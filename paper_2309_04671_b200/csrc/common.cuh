@@ -57,6 +57,8 @@ struct StarArgs {
     int32_t order_y_fast;      // work items walk y tiles fastest
     int32_t band_rows;         // > 0: items walk bands of this many tile rows, every chunk of a band
                                // before the next band (a band is about one wave of CTAs)
+    const int32_t* halo_nz;    // src buffer's halo flag: 0 = its halo is all +0, so the producer reads
+                               // through the interior-only tensor map (TMA zero-fills the halo, no DRAM)
     // fused halo exchange (multi-GPU z-slabs): src planes q < 0 are read by TMA
     // straight from the lower neighbour's buffer (its plane pull_lo_n0 + q) when
     // bit 0 of `pull` is set, planes q >= n0 from the upper neighbour's (plane q - n0)
@@ -178,7 +180,8 @@ struct StarLaunch {
     int kind;          // 1 = STAR, 2 = WAVE, 4 = BOX
     int radius;
     bool has_divisor;
-    const CUtensorMap* maps;  // [6]: src halo box, src/prev/vel centre boxes, lower/upper neighbour halo boxes
+    const CUtensorMap* maps;  // [7]: src halo box, src/prev/vel centre boxes, lower/upper neighbour halo boxes,
+                              // src halo box over the interior only
     int box_w, box_h;  // halo box the tensor maps were encoded with (must equal the kernel's tile)
     int num_sms;
     int max_ctas;      // 0 = auto (one per SM)

@@ -74,7 +74,8 @@ int fail(int code, const std::string& msg) {
 constexpr int kMaxTags = 64;
 constexpr int kMaxMaps = 256;
 constexpr int kFrozenFlag = kMaxTags + 2 * kMaxMaps;  // d_flags slot: v's frozen ring is not all zero
-constexpr int kNumFlags = kFrozenFlag + 4;
+constexpr int kHaloFlag = kFrozenFlag + 4;            // per buffer: its halo may hold non-zero values
+constexpr int kNumFlags = kHaloFlag + 40;
 
 struct MapOp {
     stkb_map_desc d;
@@ -158,6 +159,11 @@ struct stkb_domain {
     int64_t tb_pair_epoch = -1;    // ext_writes when bufs[tb_pair[0]] / [1] last had equal frozen parts
     int tb_pair[2] = {-1, -1};
     std::map<std::pair<int, int>, cudaGraphExec_t> tb_graphs;  // (u buffer, scratch) -> 2 fused passes
+    // halo flags (d_flags[kHaloFlag + buffer]): 0 = that buffer's halo is all +0, so its stencil
+    // reads go through an interior-only tensor map; recomputed when ext_writes moved
+    int64_t halo_epoch = 0;
+    bool halo_external = false;  // z-slab machinery writes halo planes (exchange, peers): full maps only
+    std::map<std::tuple<int, int, int>, CUtensorMap> tmaps_int;  // (buffer, box w, box h), interior only
 };
 
 namespace {
@@ -191,6 +197,35 @@ int encode_tmap(stkb_domain* dom, void* base, int64_t n0, int bw, int bh, CUtens
     return STKB_OK;
 }
 
+// the same box over the interior only (origin at interior (0,0,0), extents n2 x n1 x n0):
+// the TMA zero-fills every coordinate in the halo instead of reading it
+int encode_map_int(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap** out) {
+    auto key = std::make_tuple(buffer, bw, bh);
+    auto it = dom->tmaps_int.find(key);
+    if (it != dom->tmaps_int.end()) {
+        *out = &it->second;
+        return STKB_OK;
+    }
+    int rc = get_encoder();
+    if (rc) return rc;
+    const Geometry& g = dom->g;
+    char* base = static_cast<char*>(dom->bufs[buffer]) + size_t(g.at(0, 0, 0)) * dom->elem;  // 128-B aligned
+    cuuint64_t dims[3] = {cuuint64_t(g.n2), cuuint64_t(g.n1), cuuint64_t(g.n0)};
+    cuuint64_t strides[2] = {cuuint64_t(g.pitch * dom->elem), cuuint64_t(g.plane * dom->elem)};
+    cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(bh), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    static const CUtensorMapL2promotion promo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    CUtensorMap m;
+    CUresult r = g_encode(&m, dom->elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                          3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promo[dom->l2promo & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    auto res = dom->tmaps_int.emplace(key, m);
+    *out = &res.first->second;
+    return STKB_OK;
+}
+
 int encode_map(stkb_domain* dom, int buffer, int bw, int bh, const CUtensorMap** out) {
     auto key = std::make_tuple(buffer, bw, bh);
     auto it = dom->tmaps.find(key);
@@ -220,6 +255,31 @@ int encode_peer_map(stkb_domain* dom, int side, int buffer, int bw, int bh, cons
     if (rc) return rc;
     auto res = p.tmaps.emplace(key, m);
     *out = &res.first->second;
+    return STKB_OK;
+}
+
+// a buffer's halo flag := "may be non-zero" (its memory was handed out or written from
+// outside); the next ensure_halo_flags recomputes it
+void mark_halo_dirty(stkb_domain* dom, int buffer) {
+    ++dom->ext_writes;
+    const int n = int(dom->bufs.size());
+    for (int b = buffer < 0 ? 0 : buffer; b < (buffer < 0 ? n : buffer + 1); ++b)
+        cudaMemsetAsync(dom->d_flags + kHaloFlag + b, 0x01, sizeof(int32_t), dom->stream);
+}
+
+// recompute every buffer's halo flag after outside writes (not while the stream is being
+// captured: the flags then stay conservative, "may be non-zero")
+int ensure_halo_flags(stkb_domain* dom) {
+    if (dom->desc.ndim != 3 || dom->halo_external || dom->halo_epoch == dom->ext_writes) return STKB_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(dom->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return STKB_OK;
+    const Geometry& g = dom->g;
+    const Box inner{0, int32_t(g.n0), 0, int32_t(g.n1), 0, int32_t(g.n2)};
+    for (size_t b = 0; b < dom->bufs.size(); ++b)
+        CUDA_TRY(launch_frozen_ring(dom->desc.dtype, g, inner, int(g.order), dom->bufs[b],
+                                    dom->d_flags + kHaloFlag + b, dom->num_sms, dom->stream));
+    dom->halo_epoch = dom->ext_writes;
     return STKB_OK;
 }
 
@@ -273,6 +333,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
                     const RangeSpec& rs = RangeSpec(), bool pull = false) {
     const stkb_map_desc& d = op.d;
     if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
+    if (int rc = ensure_halo_flags(dom)) return rc;
     StarArgs<T> a{};
     a.g = dom->g;
     a.box = box_of(d);
@@ -304,15 +365,24 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
 #ifdef STKB_EXP_NOYHALO
-    int rc = encode_map(dom, sb, bx + 2 * hx, by, &m_halo);
+    const int lw = bx + 2 * hx, lh = by;
 #elif defined(STKB_EXP_NOXHALO)
-    int rc = encode_map(dom, sb, bx, by + 2 * R, &m_halo);
+    const int lw = bx, lh = by + 2 * R;
 #else
-    int rc = encode_map(dom, sb, bx + 2 * hx, by + 2 * R, &m_halo);
+    const int lw = bx + 2 * hx, lh = by + 2 * R;
 #endif
+    int rc = encode_map(dom, sb, lw, lh, &m_halo);
     if (rc) return rc;
-    CUtensorMap maps[6];
+    CUtensorMap maps[7];
     for (int i = 0; i < 6; ++i) maps[i] = *m_halo;
+    if (dom->desc.ndim == 3) {
+        const CUtensorMap* m_int = nullptr;
+        if ((rc = encode_map_int(dom, sb, lw, lh, &m_int))) return rc;
+        maps[6] = *m_int;
+        a.halo_nz = dom->halo_external ? nullptr : dom->d_flags + kHaloFlag + sb;
+    } else {
+        maps[6] = *m_halo;
+    }
     if (pull) {
         // src planes beyond this slab come straight from the neighbours' buffers
         for (int side = 0; side < 2; ++side) {
@@ -612,7 +682,8 @@ int stkb_layout(const stkb_domain* dom, int64_t* pitch, int64_t* plane, int64_t*
 int stkb_device_ptr(stkb_domain* dom, int32_t name, void** dptr) {
     if (!dom || !dptr) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_device_ptr")) return rc;
-    ++dom->ext_writes;  // the caller may write through the pointer
+    cudaSetDevice(dom->desc.device);
+    mark_halo_dirty(dom, dom->binding[name]);  // the caller may write through the pointer
     *dptr = dom->bufs[dom->binding[name]];
     return STKB_OK;
 }
@@ -624,6 +695,7 @@ int stkb_zero(stkb_domain* dom, int32_t name) {
     const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
     ++dom->ext_writes;
     CUDA_TRY(cudaMemsetAsync(dom->bufs[dom->binding[name]], 0, bytes, dom->stream));
+    CUDA_TRY(cudaMemsetAsync(dom->d_flags + kHaloFlag + dom->binding[name], 0, sizeof(int32_t), dom->stream));
     return STKB_OK;
 }
 
@@ -648,10 +720,10 @@ static bool ensure_stage(stkb_domain* dom, size_t want) {
 }
 
 static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
-    ++dom->ext_writes;
     if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_upload")) return rc;
     CUDA_TRY(cudaSetDevice(dom->desc.device));
+    mark_halo_dirty(dom, dom->binding[name]);
     const Geometry& g = dom->g;
     const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
     const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
@@ -894,6 +966,7 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
     int64_t done = 0;
     const int period = binding_period(dom);
     const bool graphs_ok = period > 0 && getenv("STKB_NO_GRAPH") == nullptr;
+    if (int rc = ensure_halo_flags(dom)) return rc;  // before the timed events
     if (const MapOp* tb = steps >= 4 ? tb_map(dom) : nullptr) {
         // fused sweeps for all but the last 2..3 steps, which run as single steps so
         // that v ends up holding its own final value
@@ -930,6 +1003,8 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
                 CUDA_TRY(cudaMemcpyAsync(dom->bufs[dom->scratch], dom->bufs[ub], bytes, cudaMemcpyDeviceToDevice,
                                          dom->stream));
             }
+            CUDA_TRY(cudaMemcpyAsync(dom->d_flags + kHaloFlag + dom->scratch, dom->d_flags + kHaloFlag + ub,
+                                     sizeof(int32_t), cudaMemcpyDeviceToDevice, dom->stream));  // same halo
             dom->tb_pair[0] = ub;
             dom->tb_pair[1] = dom->scratch;
             dom->tb_pair_epoch = dom->ext_writes;
@@ -1146,6 +1221,9 @@ int stkb_peer_fetch_halo(stkb_domain* dom, void* stream, int32_t planes) {
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dom->stream;
     ++dom->ext_writes;
+    dom->halo_external = true;
+    for (int b = 0; b < dom->desc.n_grids; ++b)  // my halo planes now hold the neighbours' data
+        CUDA_TRY(cudaMemsetAsync(dom->d_flags + kHaloFlag + b, 0x01, sizeof(int32_t), s));
     const size_t pb = size_t(dom->g.plane) * dom->elem;
     for (int side = 0; side < 2; ++side) {
         const auto& p = dom->peer[side];
@@ -1223,6 +1301,7 @@ int stkb_set_peer(stkb_domain* dom, int32_t side, int32_t n_bufs, void* const* b
     if (peer_n0 < dom->g.order0) return fail(STKB_ERR_ARG, "a neighbour slab must hold at least `order` planes");
     p.bufs.assign(bufs, bufs + n_bufs);
     p.tmaps.clear();
+    dom->halo_external = true;
     p.flags = static_cast<int32_t*>(flags);
     p.n0 = peer_n0;
     p.set = true;
@@ -1331,7 +1410,9 @@ int stkb_apply_swap(stkb_domain* dom, int32_t a, int32_t b) {
 int stkb_plane_span(stkb_domain* dom, int32_t name, int64_t z0, int64_t nplanes, void** dptr, int64_t* bytes) {
     if (!dom || !dptr || !bytes) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_plane_span")) return rc;
-    ++dom->ext_writes;
+    cudaSetDevice(dom->desc.device);
+    mark_halo_dirty(dom, dom->binding[name]);
+    dom->halo_external = true;  // views for the halo exchange
     const Geometry& g = dom->g;
     if (nplanes < 0 || z0 < -g.order0 || z0 + nplanes > g.n0 + g.order0)
         return fail(STKB_ERR_ARG, "plane span outside the padded grid");

@@ -58,7 +58,8 @@ struct TbCfg {
 template <typename T, int R, int TY2, int NW, bool DIV>
 __global__ void __launch_bounds__((NW + 1) * 32, 1)
 star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_v,
-                const __grid_constant__ StarArgs<T> a, const int32_t* __restrict__ frozen_nz) {
+                const __grid_constant__ CUtensorMap tm_int, const __grid_constant__ StarArgs<T> a,
+                const int32_t* __restrict__ frozen_nz) {
     using C = TbCfg<T, R, TY2, NW>;
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, TY1 = C::TY1;
     constexpr int STAGES = C::STAGES;
@@ -88,7 +89,12 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     if (warp == NW) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
-            prefetch_tmap(&tm_src);
+            // u's halo all zero: read through the interior-only map (TMA zero-fills the halo)
+            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            const CUtensorMap* um = interior ? &tm_int : &tm_src;
+            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                      iz = interior ? int(a.g.order0) : 0;
+            prefetch_tmap(um);
             prefetch_tmap(&tm_v);
             // v's frozen values around the box are all zero (the usual zero halo): no v tiles
             const bool need_v = *reinterpret_cast<const volatile int32_t*>(frozen_nz) != 0;
@@ -124,7 +130,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                     mbar_arrive_expect_tx(&full[s], C::HALO_BYTES + (vload ? C::V_BYTES : 0u));
                     // planes beyond the allocation (q < -order0 or q >= n0 + order0) are
                     // zero-filled by the TMA unit; stage 1 never uses them inside the region
-                    tma_load_3d(st, &tm_src, &full[s], c0, c1, q + int(a.g.order0));
+                    tma_load_3d(st, um, &full[s], c0 - ix, c1 - iy, q + int(a.g.order0) - iz);
                     if (vload)
                         tma_load_3d(st + C::U_ELEMS, &tm_v, &full[s], int(a.g.lead) + x0 - VEC,
                                     y0 + int(a.g.order) - R, qv + int(a.g.order0));
@@ -525,7 +531,7 @@ cudaError_t launch_tb2_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap
     const int grid = a.n_items < ctas ? a.n_items : ctas;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(map[0], map[1], a, L.frozen_nz);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(map[0], map[1], map[2], a, L.frozen_nz);
     return cudaGetLastError();
 }
 

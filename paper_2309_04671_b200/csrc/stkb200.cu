@@ -537,7 +537,10 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     const CUtensorMap *m_halo = nullptr, *m_v = nullptr;
     if (int rc = encode_map(dom, ub, bw, bh, &m_halo)) return rc;
     if (int rc = encode_map(dom, vb, vw, vh, &m_v)) return rc;
-    CUtensorMap maps[2] = {*m_halo, *m_v};
+    const CUtensorMap* m_int = nullptr;
+    if (int rc = encode_map_int(dom, ub, bw, bh, &m_int)) return rc;
+    a.halo_nz = dom->halo_external ? nullptr : dom->d_flags + kHaloFlag + ub;
+    CUtensorMap maps[3] = {*m_halo, *m_v, *m_int};
     StarLaunch L{};
     L.kind = d.kind;
     L.radius = R;

@@ -525,7 +525,11 @@ cudaError_t launch_tb2_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap
     a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper, a.zs, 0);
     a.n_signal = 0;
     a.order_y_fast = 0;
-    a.band_rows = 0;
+    a.band_rows = 0;  // item order: tile-row bands of ~one wave (as star_kernels.cuh launch_star_cfg)
+    if (L.band_pct > 0 && a.n_tx > 0) {
+        const int rows = std::max(1, (ctas * L.band_pct / 100) / a.n_tx);
+        if (rows < a.n_ty) a.band_rows = rows;
+    }
     a.n_items = tiles * a.n_tz;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;

@@ -546,6 +546,7 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     L.radius = R;
     L.has_divisor = d.divisor != 0.0;
     L.maps = maps;
+    L.band_pct = dom->band_pct;
     L.frozen_nz = dom->d_flags + kFrozenFlag;
     L.box_w = bw;
     L.box_h = bh;

@@ -185,6 +185,11 @@ int stkb_set_fused_steps(stkb_domain *dom, int32_t enable);
  * (slabs.connect_local, the peer-pull probe); IPC-opened memory does not need it. */
 int stkb_enable_peer(int32_t device, int32_t peer);
 
+/* Bring the per-buffer halo flags up to date after outside writes (normally done by the
+ * next uncaptured launch): call before capturing launches into a CUDA graph so the captured
+ * kernels can read zero halos through interior-only tensor maps. */
+int stkb_prepare(stkb_domain *dom);
+
 /* Fused halo exchange over NVLink peer memory (z-slab neighbours, one process
  * per GPU).  Each rank exports its buffers and its 2-slot flag array with CUDA
  * IPC handles (64 bytes), opens its neighbours' with stkb_ipc_open and

@@ -35,7 +35,7 @@ EXPORTS = (
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
     "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
     "stkb_flags_ipc_handle", "stkb_buffer_ptr", "stkb_flags_ptr", "stkb_ipc_open", "stkb_ipc_close", "stkb_set_peer",
-    "stkb_peer_signal", "stkb_peer_wait", "stkb_set_fused_steps", "stkb_enable_peer",
+    "stkb_peer_signal", "stkb_peer_wait", "stkb_set_fused_steps", "stkb_enable_peer", "stkb_prepare",
 )
 
 
@@ -134,6 +134,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_set_max_ctas": [V, i32],
         "stkb_set_fused_steps": [V, i32],
         "stkb_enable_peer": [i32, i32],
+        "stkb_prepare": [V],
         "stkb_launch_map_pull": [V, i32],
         "stkb_peer_fetch_halo": [V, V, i32],
         "stkb_buffer_ipc_handle": [V, i32, V],

@@ -18,11 +18,11 @@ cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaS
 }
 
 cudaError_t launch_frozen_ring(int dtype, const Geometry& g, const Box& b, int R, const void* buf, int32_t* flag,
-                               int num_sms, cudaStream_t s) {
+                               int num_sms, cudaStream_t s, int zmask) {
     cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
-    if (dtype == 1) frozen_ring_kernel<float><<<2 * num_sms, 256, 0, s>>>(static_cast<const float*>(buf), g, b, R, flag);
-    else frozen_ring_kernel<double><<<2 * num_sms, 256, 0, s>>>(static_cast<const double*>(buf), g, b, R, flag);
+    if (dtype == 1) frozen_ring_kernel<float><<<2 * num_sms, 256, 0, s>>>(static_cast<const float*>(buf), g, b, R, flag, zmask);
+    else frozen_ring_kernel<double><<<2 * num_sms, 256, 0, s>>>(static_cast<const double*>(buf), g, b, R, flag, zmask);
     return cudaGetLastError();
 }
 

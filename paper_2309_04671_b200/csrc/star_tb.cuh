@@ -464,9 +464,11 @@ struct TbTile {
 };
 
 // *flag |= 1 when a cell of `buf` within R of the box (along any axis, outside it) is not
-// bit-for-bit +0: the fused sweep then stages v's frozen values through TMA
+// bit-for-bit +0: the fused sweep then stages v's frozen values through TMA.  zmask bit 0 / 1:
+// check the d0 face below / above the box (a z-slab side whose planes come from a neighbour
+// is left out)
 template <typename T>
-__global__ void frozen_ring_kernel(const T* __restrict__ buf, Geometry g, Box b, int R, int32_t* flag) {
+__global__ void frozen_ring_kernel(const T* __restrict__ buf, Geometry g, Box b, int R, int32_t* flag, int zmask) {
     const int64_t X = int64_t(b.hi2 - b.lo2) + 2 * R, Y = int64_t(b.hi1 - b.lo1) + 2 * R;
     const int64_t nz = int64_t(b.hi0 - b.lo0), ny = int64_t(b.hi1 - b.lo1), nx = int64_t(b.hi2 - b.lo2);
     const int64_t nA = 2 * R * Y * X, nB = nz * 2 * R * X, nC = nz * ny * 2 * R;
@@ -476,6 +478,7 @@ __global__ void frozen_ring_kernel(const T* __restrict__ buf, Geometry g, Box b,
         int64_t z, y, x;
         if (i < nA) {  // planes below / above the box
             const int64_t k = i / (Y * X), r = i - k * Y * X;
+            if (!(zmask & (k < R ? 1 : 2))) continue;
             z = k < R ? b.lo0 - R + k : b.hi0 + (k - R);
             y = b.lo1 - R + r / X;
             x = b.lo2 - R + r % X;

@@ -47,7 +47,7 @@ cudaError_t launch_tb2_f32(const StarLaunch& L, const StarArgs<float>& a, cudaSt
 cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
 int tb2_tile(int dtype, int radius, int* box_w, int* box_h, int* v_w, int* v_h);
 cudaError_t launch_frozen_ring(int dtype, const Geometry& g, const Box& b, int R, const void* buf, int32_t* flag,
-                               int num_sms, cudaStream_t s);
+                               int num_sms, cudaStream_t s, int zmask = 3);
 cudaError_t launch_copy_halo(const void* src, void* dst, const Geometry& g, int esz, int num_sms, cudaStream_t s);
 cudaError_t launch_star2d(int dtype, const Star2DArgs& a, int R, const void* src, void* dst, bool div, int num_sms,
                           cudaStream_t s);
@@ -276,9 +276,12 @@ int ensure_halo_flags(stkb_domain* dom) {
     if (cs != cudaStreamCaptureStatusNone) return STKB_OK;
     const Geometry& g = dom->g;
     const Box inner{0, int32_t(g.n0), 0, int32_t(g.n1), 0, int32_t(g.n2)};
+    // a z-slab side with a fused-exchange neighbour never reads its own halo planes (the
+    // pulling kernels fetch those planes from the neighbour): leave that face out
+    const int zmask = (dom->peer[0].set ? 0 : 1) | (dom->peer[1].set ? 0 : 2);
     for (size_t b = 0; b < dom->bufs.size(); ++b)
         CUDA_TRY(launch_frozen_ring(dom->desc.dtype, g, inner, int(g.order), dom->bufs[b],
-                                    dom->d_flags + kHaloFlag + b, dom->num_sms, dom->stream));
+                                    dom->d_flags + kHaloFlag + b, dom->num_sms, dom->stream, zmask));
     dom->halo_epoch = dom->ext_writes;
     return STKB_OK;
 }
@@ -1299,13 +1302,14 @@ int stkb_set_peer(stkb_domain* dom, int32_t side, int32_t n_bufs, void* const* b
     auto& p = dom->peer[side];
     if (!bufs) {  // detach
         p = stkb_domain::Peer();
+        ++dom->ext_writes;
         return STKB_OK;
     }
     if (n_bufs != dom->desc.n_grids || !flags) return fail(STKB_ERR_ARG, "peer needs one pointer per buffer and its flags");
     if (peer_n0 < dom->g.order0) return fail(STKB_ERR_ARG, "a neighbour slab must hold at least `order` planes");
     p.bufs.assign(bufs, bufs + n_bufs);
     p.tmaps.clear();
-    dom->halo_external = true;
+    ++dom->ext_writes;  // halo flags: this side's z face no longer counts
     p.flags = static_cast<int32_t*>(flags);
     p.n0 = peer_n0;
     p.set = true;
@@ -1374,6 +1378,12 @@ int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, i
                          cuuint32_t(value), CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(STKB_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(int(r)));
     return STKB_OK;
+}
+
+int stkb_prepare(stkb_domain* dom) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    return ensure_halo_flags(dom);
 }
 
 int stkb_enable_peer(int32_t device, int32_t peer) {

@@ -432,6 +432,9 @@ class DeviceSlabEngine:
                 key = (self.binding(), self.t % 3)
                 hit = self.graphs.get(key)
                 if hit is None:
+                    from . import _lib as L
+
+                    L.call("stkb_prepare", self.dt.h)  # halo flags current before capturing
                     # capture without a device synchronisation (other ranks' streams may be
                     # waiting on this one): record `period` steps, which does not run them
                     g = torch.cuda.CUDAGraph()

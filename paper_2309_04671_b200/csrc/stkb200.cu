@@ -149,6 +149,7 @@ struct stkb_domain {
     int store_hint = 0;   // STKB_STORE_HINT: 0 default, 1 streaming (.cs) stores
     bool taper = true;    // STKB_TAPER=0 disables the shortened final z-chunks
     int order_y_fast = 0; // STKB_ORDER_Y=1: work items walk y tiles fastest
+    bool prescale = false; // STKB_PRESCALE=1: fold a Jacobi divisor into the coefficients (fill_coefs)
     int band_pct = 100;   // STKB_BAND: item order in tile-row bands of this % of a wave (0: z-major; StarArgs::band_rows)
     // two time steps per sweep (star_tb.cuh) for the Jacobi ping-pong of a radius <= 2 star:
     // u(t+2) goes to a scratch buffer bufs[scratch] and u's binding rotates with it
@@ -286,6 +287,25 @@ int ensure_halo_flags(stkb_domain* dom) {
     return STKB_OK;
 }
 
+// star coefficients into the kernel arguments.  A divisor (Jacobi `/d`) is either applied
+// by the kernel as a multiply by 1/d after the sum (returns true), or — `prescale` — folded
+// into the coefficients on the host in float64 (returns false: one multiply less per point;
+// same tolerance, different rounding)
+template <typename T>
+bool fill_coefs(StarArgs<T>& a, const stkb_map_desc& d, bool prescale) {
+    const int R = d.radius;
+    const bool fold = prescale && d.divisor != 0.0;
+    const double sc = fold ? 1.0 / d.divisor : 1.0;
+    a.c0 = T(d.coef[0] * sc);
+    for (int ax = 0; ax < 3; ++ax)
+        for (int m = 1; m <= 4; ++m) {
+            a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)] * sc) : T(0);
+            a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1] * sc) : T(0);
+        }
+    a.divisor = d.divisor != 0.0 && !fold ? T(1.0 / d.divisor) : T(0);  // the kernel multiplies by it
+    return d.divisor != 0.0 && !fold;
+}
+
 Box box_of(const stkb_map_desc& d) {
     Box b;
     b.lo0 = int32_t(d.lo[0]); b.hi0 = int32_t(d.hi[0]);
@@ -350,19 +370,15 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
     a.work_counter = dom->d_flags + kMaxTags + op.slot;
     const int R = d.radius;
-    a.c0 = T(d.coef[0]);
-    for (int ax = 0; ax < 3; ++ax)
-        for (int m = 1; m <= 4; ++m) {
-            a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)]) : T(0);
-            a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1]) : T(0);
-        }
-    a.divisor = d.divisor != 0.0 ? T(1.0 / d.divisor) : T(0);  // the kernel multiplies by the reciprocal
+    const bool div = fill_coefs(a, d, dom->prescale);
     a.wave_a = T(d.wave_a);
     a.wave_b = T(d.wave_b);
     a.store_hint = dom->store_hint;
     a.order_y_fast = dom->order_y_fast;
-    if (d.kind == STKB_MAP_BOX)
-        for (size_t i = 0; i < op.cube.size(); ++i) a.cb[i] = T(op.cube[i]);
+    if (d.kind == STKB_MAP_BOX) {
+        const double sc = div || d.divisor == 0.0 ? 1.0 : 1.0 / d.divisor;  // prescaled: fold 1/d in
+        for (size_t i = 0; i < op.cube.size(); ++i) a.cb[i] = T(op.cube[i] * sc);
+    }
 
     int bx, by, hx;
     star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
@@ -409,7 +425,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     StarLaunch L{};
     L.kind = d.kind;
     L.radius = R;
-    L.has_divisor = d.divisor != 0.0;
+    L.has_divisor = div;
     L.maps = maps;
     L.box_w = bx + 2 * hx;
     L.box_h = by + 2 * R;  // (STKB_EXP_NOYHALO loads fewer rows; the stage keeps this shape)
@@ -528,13 +544,7 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     a.nonfinite = dom->d_flags + (d.tag & (kMaxTags - 1));
     a.work_counter = dom->d_flags + kMaxTags + op.slot;
     const int R = d.radius;
-    a.c0 = T(d.coef[0]);
-    for (int ax = 0; ax < 3; ++ax)
-        for (int m = 1; m <= 4; ++m) {
-            a.cm[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1)]) : T(0);
-            a.cp[ax][m - 1] = m <= R ? T(d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1]) : T(0);
-        }
-    a.divisor = d.divisor != 0.0 ? T(1.0 / d.divisor) : T(0);
+    const bool div = fill_coefs(a, d, dom->prescale);
     int bw, bh, vw, vh;
     if (tb2_tile(dom->desc.dtype, R, &bw, &bh, &vw, &vh)) return fail(STKB_ERR_UNSUPPORTED, "fused sweep radius");
     const CUtensorMap *m_halo = nullptr, *m_v = nullptr;
@@ -547,7 +557,7 @@ int launch_tb2_map(stkb_domain* dom, const MapOp& op) {
     StarLaunch L{};
     L.kind = d.kind;
     L.radius = R;
-    L.has_divisor = d.divisor != 0.0;
+    L.has_divisor = div;
     L.maps = maps;
     L.band_pct = dom->band_pct;
     L.frozen_nz = dom->d_flags + kFrozenFlag;
@@ -650,6 +660,7 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_TAPER")) dom->taper = atoi(s) != 0;
     if (const char* s = getenv("STKB_ORDER_Y")) dom->order_y_fast = atoi(s);
     if (const char* s = getenv("STKB_BAND")) dom->band_pct = atoi(s);
+    if (const char* s = getenv("STKB_PRESCALE")) dom->prescale = atoi(s) != 0;
     if (const char* s = getenv("STKB_TB")) dom->tb = atoi(s) != 0;
     *out = dom;
     return STKB_OK;

@@ -312,7 +312,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     while (true) {
         // the producer tags every stage with its work item; -1 ends the kernel
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
-        const int item = stage_item[it % STAGES];
+        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);  // warp-uniform: uniform branches
         if (item < 0) break;
         int tx, ty, tz;
         decode_item(a, item, tx, ty, tz);

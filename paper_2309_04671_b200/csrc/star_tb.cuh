@@ -168,7 +168,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
-        const int item = stage_item[it % STAGES];
+        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);  // warp-uniform
         if (item < 0) break;
         int tx, ty, tz;
         decode_item(a, item, tx, ty, tz);

@@ -514,7 +514,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     }
                     // every shared read of stage s is done: hand it back to the producer
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s]);
+                    mbar_arrive_lane0(&empty[s], lane);
                     ++it;
 
                     if (z_out) {

@@ -406,7 +406,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                         // -------- u(t+2) plane z = qv - R is complete
                         const int z = qv - R;
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&empty[s]);
+                        mbar_arrive_lane0(&empty[s], lane);
                         if (z >= z0 && z < z1) {
                             T outv[TY2][VEC];
 #pragma unroll
@@ -437,7 +437,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                         }
                     } else {
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&empty[s]);
+                        mbar_arrive_lane0(&empty[s], lane);
                     }
                     ++it;
                 }

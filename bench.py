@@ -77,15 +77,31 @@ class ClockSampler:
         try:
             self.out = open(f"/tmp/stkb_clocks_{os.getpid()}.csv", "w+")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "25"],
                                          stdout=self.out, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
-        time.sleep(0.25)
+        # the timed region starts only once the sampler is producing lines (its start-up time
+        # varies; a short timed region could otherwise pass unsampled)
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 10.0:
+            self.out.flush()
+            if os.path.getsize(self.out.name) > 0:
+                break
+            time.sleep(0.02)
+        self.lines_before = self._count()
         return self
+
+    def _count(self) -> int:
+        try:
+            with open(self.out.name) as f:
+                return sum(1 for _ in f)
+        except OSError:
+            return 0
 
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.05)  # the sample that covers the end of the timed region
             self.proc.terminate()
             self.proc.wait()
 
@@ -95,7 +111,11 @@ class ClockSampler:
         self.out.seek(0)
         sms, maxes, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.out.read().splitlines():
+        # samples taken while the timed region ran (the lines before it are the sampler's
+        # start-up); all of them if the region was shorter than one sampling interval
+        lines = self.out.read().splitlines()
+        during = lines[getattr(self, "lines_before", 0):]
+        for line in during if during else lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue

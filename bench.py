@@ -336,7 +336,7 @@ def run_ours(args) -> None:
 
     # ------------------------------------------------------------ CPU baseline
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N=1 only
         try:
             from oracle import ref_runner
 

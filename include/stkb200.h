@@ -128,7 +128,13 @@ int stkb_domain_create(const stkb_domain_desc *desc, stkb_domain **out);
 int stkb_domain_destroy(stkb_domain *dom);
 int stkb_layout(const stkb_domain *dom, int64_t *pitch_elems, int64_t *plane_elems,
                 int64_t *lead_elems, int64_t *buffer_elems);
+/* Raw device pointer of the buffer bound to `name`.  Handing it out marks that buffer
+ * "written from outside" (halo flag and fused-sweep scratch are re-derived at the next
+ * stkb_run*).  Writes through a pointer kept across runs must be followed by
+ * stkb_mark_dirty(name) (or a fresh stkb_device_ptr) before the next stkb_run*, or the
+ * kernels may read a stale "halo is zero" flag. */
 int stkb_device_ptr(stkb_domain *dom, int32_t name, void **dptr);
+int stkb_mark_dirty(stkb_domain *dom, int32_t name);
 int stkb_set_stream(stkb_domain *dom, void *cuda_stream); /* NULL = domain's own */
 int stkb_zero(stkb_domain *dom, int32_t name);            /* whole buffer (halo, padding) = 0, async */
 

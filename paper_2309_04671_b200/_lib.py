@@ -28,7 +28,7 @@ EXPR_MAX_ARGS, EXPR_MAX_LOCALS, EXPR_MAX_STACK = 8, 16, 32
 # every entry point include/stkb200.h declares
 EXPORTS = (
     "stkb_abi_version", "stkb_last_error", "stkb_device_count", "stkb_domain_create",
-    "stkb_domain_destroy", "stkb_layout", "stkb_device_ptr", "stkb_zero", "stkb_set_stream", "stkb_upload",
+    "stkb_domain_destroy", "stkb_layout", "stkb_device_ptr", "stkb_mark_dirty", "stkb_zero", "stkb_set_stream", "stkb_upload",
     "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_program_reset",
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
@@ -108,6 +108,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_domain_destroy": [V],
         "stkb_layout": [V, P(i64), P(i64), P(i64), P(i64)],
         "stkb_device_ptr": [V, i32, P(V)],
+        "stkb_mark_dirty": [V, i32],
         "stkb_zero": [V, i32],
         "stkb_set_stream": [V, V],
         "stkb_upload": [V, i32, V],

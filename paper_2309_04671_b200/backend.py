@@ -170,6 +170,11 @@ class DeviceTarget:
         L.call("stkb_device_ptr", self.h, self.index[name], ctypes.byref(p))
         return p.value
 
+    def mark_dirty(self, name: str) -> None:
+        """Declare writes through a device pointer fetched before the last run
+        (include/stkb200.h stkb_mark_dirty)."""
+        L.call("stkb_mark_dirty", self.h, self.index[name])
+
     def set_stream(self, stream_handle: int) -> None:
         L.call("stkb_set_stream", self.h, ctypes.c_void_p(stream_handle or None))
 
@@ -487,9 +492,13 @@ def dead_on_entry(stmts, names, bindings: dict, shape=None) -> set:
 
 
 def halo_is_zero(g) -> bool:
-    d, o = g.data, g.order
+    """Is every halo element +0.0 bit for bit (-0.0 is not: the reference copies halos
+    through unchanged, and a fresh device grid holds +0.0)?"""
+    o = g.order
     if o == 0:
         return True
+    d = np.ascontiguousarray(g.data)
+    d = d.view(np.uint32 if d.dtype.itemsize == 4 else np.uint64)
     nd = d.ndim
     for ax in range(nd):
         lo = [slice(None)] * nd

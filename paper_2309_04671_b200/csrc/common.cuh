@@ -5,6 +5,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current device only:
+// `mask` (one static per kernel instantiation) records the devices it was set on
+template <typename K>
+inline cudaError_t ensure_smem_attr(K kern, int smem, uint64_t& mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (mask & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) mask |= bit;
+    return e;
+}
+
 namespace stkb {
 
 // ---------------------------------------------------------------------------

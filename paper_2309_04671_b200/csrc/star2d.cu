@@ -232,12 +232,8 @@ cudaError_t launch2d_rb(const Star2DArgs& a, const Coef2D<T>& cf, const void* sr
     const int blocks = (warps + Ring2D<T, R>::WARPS - 1) / Ring2D<T, R>::WARPS;
     constexpr size_t smem = Ring2D<T, R>::SMEM;
     auto kern = div ? star2d_kernel<T, R, true, BOX> : star2d_kernel<T, R, false, BOX>;
-    static bool attr_set[2] = {false, false};  // per instantiation pair
-    if (!attr_set[div]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        attr_set[div] = true;
-    }
+    static uint64_t attr_devices[2] = {0, 0};  // per instantiation pair, per device
+    if (cudaError_t e = ensure_smem_attr(kern, int(smem), attr_devices[div])) return e;
     kern<<<blocks, 32 * Ring2D<T, R>::WARPS, smem, s>>>(static_cast<const T*>(src), static_cast<T*>(dst), a, cf);
     return cudaGetLastError();
 }

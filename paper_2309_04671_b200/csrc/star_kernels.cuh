@@ -623,12 +623,8 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     // a tensor-map box that differs from this instantiation's tile would make the
     // mbarrier transaction counts disagree (a hang): refuse instead
     if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static uint64_t attr_devices = 0;  // per instantiation, per device
+    if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
     const int w2 = a.box.hi2 - a.x0base;
     a.n_tx = (w2 + C::BX - 1) / C::BX;
     a.n_ty = (a.box.hi1 - a.box.lo1 + C::BY - 1) / C::BY;

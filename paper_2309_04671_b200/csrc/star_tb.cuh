@@ -507,12 +507,8 @@ cudaError_t launch_tb2_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap
     using C = TbCfg<T, R, TY2, NW>;
     auto kern = star_tb2_kernel<T, R, TY2, NW, DIV>;
     if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static uint64_t attr_devices = 0;  // per instantiation, per device
+    if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
     a.n_tx = (a.box.hi2 - a.x0base + C::BX - 1) / C::BX;
     a.n_ty = (a.box.hi1 - a.box.lo1 + C::BY - 1) / C::BY;
     const int n0 = a.box.hi0 - a.box.lo0;

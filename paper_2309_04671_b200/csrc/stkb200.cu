@@ -493,6 +493,9 @@ void invalidate_graph(stkb_domain* dom) {
     for (auto& kv : dom->tb_graphs) cudaGraphExecDestroy(kv.second);
     dom->tb_graphs.clear();
     dom->tb_warmed = false;
+    // a new program may write u or the scratch outside the fused map's box: the pair no
+    // longer agrees there
+    dom->tb_pair_epoch = -1;
     dom->gperiod = 0;
     dom->warmed = false;
 }
@@ -703,6 +706,14 @@ int stkb_device_ptr(stkb_domain* dom, int32_t name, void** dptr) {
     cudaSetDevice(dom->desc.device);
     mark_halo_dirty(dom, dom->binding[name]);  // the caller may write through the pointer
     *dptr = dom->bufs[dom->binding[name]];
+    return STKB_OK;
+}
+
+int stkb_mark_dirty(stkb_domain* dom, int32_t name) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (int rc = check_name(dom, name, "stkb_mark_dirty")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    mark_halo_dirty(dom, dom->binding[name]);
     return STKB_OK;
 }
 
@@ -1106,6 +1117,7 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
 
 int stkb_run_once(stkb_domain* dom) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     int64_t launches = 0;
     CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
@@ -1157,6 +1169,7 @@ int stkb_nonfinite(stkb_domain* dom, int32_t tag, int32_t* flag) {
 
 int stkb_launch_map(stkb_domain* dom, int32_t map_index, int64_t lo0, int64_t hi0) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     MapOp& op = dom->maps[map_index];
@@ -1176,6 +1189,7 @@ int stkb_launch_map(stkb_domain* dom, int32_t map_index, int64_t lo0, int64_t hi
 int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges, const int64_t* lo0,
                            const int64_t* hi0, int32_t n_signal, int32_t* signal_items) {
     if (!dom || (n_ranges > 0 && (!lo0 || !hi0))) return fail(STKB_ERR_ARG, "null argument");
+    dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     if (n_ranges < 0 || n_ranges > 64 || n_signal < 0 || n_signal > n_ranges)
         return fail(STKB_ERR_ARG, "bad range list");
@@ -1224,6 +1238,7 @@ int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges
 
 int stkb_launch_map_pull(stkb_domain* dom, int32_t map_index) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     MapOp& op = dom->maps[map_index];
     if (op.d.kind == STKB_MAP_EXPR || dom->desc.ndim != 3)

@@ -194,3 +194,7 @@ def test_dead_inputs_detected():
     assert halo_is_zero(g)
     g.data[0, 3, 3] = 1.0
     assert not halo_is_zero(g)
+    g.data[0, 3, 3] = -0.0  # equal to 0.0 numerically, not bit for bit: must be uploaded
+    assert not halo_is_zero(g)
+    g.data[0, 3, 3] = 0.0
+    assert halo_is_zero(g)

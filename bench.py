@@ -187,7 +187,7 @@ def pinned_grids(decls, builder, seed=7):
     """GridBuffers whose data live in pinned host memory (e2e inputs)."""
     import torch
 
-    from paper_2309_04671_b200.grids import GridBuffer
+    from paper_2309_04671_b200 import GridBuffer
 
     out = {}
     for n, d in decls.items():
@@ -210,7 +210,7 @@ def run_ours(args) -> None:
 
     from paper_2309_04671_b200 import DeviceTarget, run_gpu
     from paper_2309_04671_b200 import corpus
-    from paper_2309_04671_b200.planning import plan_gpu
+    from paper_2309_04671_b200 import plan_gpu
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -395,7 +395,7 @@ def run_ours(args) -> None:
 
 
 def _decl_grid(d):
-    from paper_2309_04671_b200.grids import GridBuffer
+    from paper_2309_04671_b200 import GridBuffer
 
     return GridBuffer(d.dtype, tuple(d.shape), d.order, np.zeros((1,) * len(d.shape), np.float32))
 

@@ -72,13 +72,16 @@ extern "C" {
 
 typedef struct stkb_domain stkb_domain;
 
-/* One domain = n_grids named grids sharing dtype, logical shape and halo
- * order (GridBuffer, grids.py:20-64).  Device layout is pitched: a row of the
- * contiguous dim d2 starts on a 128-byte boundary and the first interior
- * element of each row sits at `lead` elements (128 bytes) into the row. */
+/* One domain = n_grids named grids sharing dtype and one device geometry: the
+ * largest interior extents and halo order of the target's grids (GridBuffer,
+ * grids.py:20-64; the grids of one target may differ in order and shape,
+ * parser.py:681-691 — see stkb_upload_grid).  Device layout is pitched: a row of
+ * the contiguous dim d2 starts on a 128-byte boundary and the first interior
+ * element of each row sits at `lead` elements (128 bytes) into the row.  1-D grids
+ * are one row of one plane, 2-D grids one plane (EXPR maps only for 1-D). */
 typedef struct {
     int32_t dtype;    /* STKB_F32 | STKB_F64 */
-    int32_t ndim;     /* 3 */
+    int32_t ndim;     /* 1, 2 or 3 */
     int64_t shape[3]; /* interior extents (d0 streaming/slab axis, d1, d2 contiguous) */
     int32_t order;    /* halo width on every side, >= every kernel radius */
     int32_t n_grids;  /* number of named grids (names are 0..n_grids-1) */
@@ -143,6 +146,15 @@ int stkb_upload(stkb_domain *dom, int32_t name, const void *host_padded);
 int stkb_download(stkb_domain *dom, int32_t name, void *host_padded);
 int stkb_upload_async(stkb_domain *dom, int32_t name, const void *host_padded);
 int stkb_download_async(stkb_domain *dom, int32_t name, void *host_padded);
+/* The same for a grid with its own layout: host_padded is C-order with
+ * (shape[d] + 2*order) elements per axis (the domain's ndim axes); shape[d] <= the
+ * domain's extents and order <= the domain's order.  Its interior origin is the
+ * domain's; after an upload every device cell outside its padded box is +0.0.
+ * sync != 0 waits for the copy. */
+int stkb_upload_grid(stkb_domain *dom, int32_t name, const void *host_padded, const int64_t *shape,
+                     int32_t order, int32_t sync);
+int stkb_download_grid(stkb_domain *dom, int32_t name, void *host_padded, const int64_t *shape,
+                       int32_t order, int32_t sync);
 
 /* step program: a sequence of maps and swaps replayed `steps` times */
 int stkb_program_reset(stkb_domain *dom);

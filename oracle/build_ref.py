@@ -35,6 +35,17 @@ SAMPLES = {
     "c5_star3d2r_norm_f64": ("star3d2r_norm", (32, 2048, 1024), "f64"),
     "c5_star3d4r_norm_f64": ("star3d4r_norm", (32, 2048, 1024), "f64"),
 }
+# full-size parity programs (tests/test_gpu_parity_full.py): the BASELINE configs at their
+# own shapes; c5 (2048 x 2048 x 1024 fp64) as d0 windows of PARITY_WINDOW planes of the
+# full grid (outputs more than steps x radius planes from a cut are exact, see the test)
+PARITY_WINDOW = 104
+PARITY = {
+    "p_c2_jacobi7": ("jacobi7", (512, 512, 512), "f32"),
+    "p_c3_wave": ("wave", (1024, 1024, 1024), "f32"),
+    "p_c4_star3d4r_norm": ("star3d4r_norm", (1024, 1024, 1024), "f32"),
+    "p_c5a_star3d2r_norm_win": ("star3d2r_norm", (PARITY_WINDOW, 2048, 1024), "f64"),
+    "p_c5b_star3d4r_norm_win": ("star3d4r_norm", (PARITY_WINDOW, 2048, 1024), "f64"),
+}
 CFLAGS = ["-O3", "-march=x86-64-v3", "-fopenmp", "-fPIC", "-shared"]
 
 
@@ -46,18 +57,7 @@ def program_text(builder: str, shape, dtype: str) -> str:
     sys.path.insert(0, str(ROOT))
     from paper_2309_04671_b200 import corpus
 
-    if builder == "wave":
-        return corpus.source_text(corpus.wave_kernel(), shape, 4, 1, dtype, swap=("up", "u"),
-                                  target="target_acoustic_iso", backend="st.omp()")
-    if builder == "jacobi7":
-        return corpus.source_text(corpus.jacobi7_kernel(), shape, 1, 1, dtype, target="target_jacobi7",
-                                  backend="st.omp()")
-    if builder.endswith("_norm"):
-        base = builder.removesuffix("_norm")
-        return corpus.source_text(corpus.normalised_star_kernel(base), shape, corpus.KERNELS[base].radius, 1,
-                                  dtype, target=f"target_{builder}", backend="st.omp()")
-    return corpus.source_text(corpus.corpus_kernel(builder), shape, corpus.KERNELS[builder].radius, 1, dtype,
-                              target=f"target_{builder}", backend="st.omp()")
+    return corpus.program_text(builder, shape, 1, dtype, backend="st.omp()")
 
 
 def build(force: bool = False) -> dict:
@@ -71,7 +71,7 @@ def build(force: bool = False) -> dict:
 
     OUT.mkdir(exist_ok=True)
     manifest = {}
-    for name, (builder, shape, dtype) in SAMPLES.items():
+    for name, (builder, shape, dtype) in {**SAMPLES, **PARITY}.items():
         text = program_text(builder, shape, dtype)
         unit = parse_source(text, f"{name}.stpy")
         assert not validate(unit)

@@ -103,6 +103,35 @@ def run(name: str, steps: int, warmup: int) -> dict:
                        f"{'x'.join(map(str, shape))} {entry['dtype']}, {steps} steps, {flags}")
 
 
+_LOADED: dict = {}
+
+
+def call(name: str, arrays: list, steps: int) -> float:
+    """Run the reference-emitted C of manifest entry ``name`` in this process on
+    caller-owned padded arrays (in target-parameter order, mutated in place: the
+    reference C-ABI, serial.py:126-208) for ``steps`` time steps; returns seconds.
+    Test infrastructure: the parity tests' oracle at BASELINE sizes."""
+    entry = load_manifest()[name]
+    if name not in _LOADED:
+        path, _ = library(entry)
+        _LOADED[name] = ctypes.CDLL(str(path))
+    fn = getattr(_LOADED[name], entry["entry"])
+    cty = ctypes.c_float if entry["dtype"] == "f32" else ctypes.c_double
+    dt = np.float32 if entry["dtype"] == "f32" else np.float64
+    order = _order(entry["builder"])
+    padded = tuple(e + 2 * order for e in entry["shape"])
+    if len(arrays) != len(entry["grids"]):
+        raise ValueError(f"{name} takes {len(entry['grids'])} grids")
+    for a in arrays:
+        if a.dtype != dt or tuple(a.shape) != padded or not a.flags.c_contiguous:
+            raise ValueError(f"{name}: arrays must be C-contiguous {dt.__name__}{padded}")
+    fn.argtypes = [ctypes.POINTER(cty)] * len(arrays) + [ctypes.c_int64]
+    fn.restype = None
+    t0 = time.perf_counter()
+    fn(*[a.ctypes.data_as(ctypes.POINTER(cty)) for a in arrays], ctypes.c_int64(steps))
+    return time.perf_counter() - t0
+
+
 def main(argv=None) -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--name", required=True)

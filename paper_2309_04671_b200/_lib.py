@@ -29,7 +29,8 @@ EXPR_MAX_ARGS, EXPR_MAX_LOCALS, EXPR_MAX_STACK = 8, 16, 32
 EXPORTS = (
     "stkb_abi_version", "stkb_last_error", "stkb_device_count", "stkb_domain_create",
     "stkb_domain_destroy", "stkb_layout", "stkb_device_ptr", "stkb_mark_dirty", "stkb_zero", "stkb_set_stream", "stkb_upload",
-    "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_program_reset",
+    "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_upload_grid", "stkb_download_grid",
+    "stkb_program_reset",
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
@@ -115,6 +116,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_download": [V, i32, V],
         "stkb_upload_async": [V, i32, V],
         "stkb_download_async": [V, i32, V],
+        "stkb_upload_grid": [V, i32, V, P(i64), i32, i32],
+        "stkb_download_grid": [V, i32, V, P(i64), i32, i32],
         "stkb_program_reset": [V],
         "stkb_program_add_map": [V, P(MapDesc)],
         "stkb_program_add_swap": [V, i32, i32],

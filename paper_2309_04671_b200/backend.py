@@ -26,24 +26,21 @@ from typing import Optional
 import numpy as np
 
 from . import _lib as L
+from . import front
+from .front import stmt_kind
 from .matcher import MapPlan, MatchError, match_map
-from .program import stmt_kind
 
 GPU_TEMPLATES = ("gmem", "smem", "f4", "shift", "unroll", "semi")
 
-
-class ExecutionError(ValueError):
-    """Mirror of executor.py:34-35 (a ValueError, exit code 1 in the CLI)."""
+# the reference's own error type (executor.py:35-36): a ValueError, exit code 1 in its CLI
+ExecutionError = front.module("executor").ExecutionError
 
 
 def _prepare(unit, target, args, scheme):
     if hasattr(unit, "stmts") and hasattr(unit, "grid_params"):
         return unit
-    try:  # a reference SourceUnit: bind it with the reference front end
-        from stencilkit.analysis import bind_target  # type: ignore
-    except ImportError:
-        raise ExecutionError("run_gpu needs a BoundTarget (the stencilkit front end is not importable)") from None
-    return bind_target(unit, target, args, scheme)
+    # a reference SourceUnit: bound by the reference front end, as executor._prepare does
+    return front.module("analysis").bind_target(unit, target, args, scheme)
 
 
 def _maps(stmts):
@@ -89,16 +86,22 @@ class DeviceTarget:
         ref = grids[self.names[0]]
         for n in self.names:
             g = grids[n]
-            if (g.dtype, tuple(g.shape), g.order) != (ref.dtype, tuple(ref.shape), ref.order):
+            if (g.dtype, len(g.shape)) != (ref.dtype, len(ref.shape)):
                 raise ExecutionError(
-                    f"grid '{n}' is {g.dtype}{tuple(g.shape)}/order {g.order}; the device domain needs every "
-                    f"grid of a target to match {ref.dtype}{tuple(ref.shape)}/order {ref.order}")
+                    f"grid '{n}' is {g.dtype} {len(g.shape)}-D; the device path needs every grid of a target in one "
+                    f"dtype and rank ({ref.dtype} {len(ref.shape)}-D)")
         if ref.dtype not in ("f32", "f64"):
             raise ExecutionError(f"unsupported dtype {ref.dtype}")
         nd = len(ref.shape)
-        if nd not in (2, 3):
+        if nd not in (1, 2, 3):
             raise ExecutionError(f"{nd}-D grids are not supported on the device")
-        self.dtype, self.shape, self.order = ref.dtype, tuple(ref.shape), ref.order
+        # one device geometry for the target: the largest extents and halo order of its
+        # grids (they may differ, parser.py:681-691); each grid keeps its own host layout
+        self.layouts = {n: (tuple(grids[n].shape), int(grids[n].order)) for n in self.names}
+        shape = tuple(max(self.layouts[n][0][d] for n in self.names) for d in range(nd))
+        order = max(o for _, o in self.layouts.values())
+        self.dtype, self.shape, self.order = ref.dtype, shape, order
+        self.uniform = all(lay == (shape, order) for lay in self.layouts.values())
         self.np_dtype = np.float32 if ref.dtype == "f32" else np.float64
         self.index = {n: i for i, n in enumerate(self.names)}
         self.grid_cls = type(ref)
@@ -108,7 +111,7 @@ class DeviceTarget:
         desc.ndim = nd
         for d, e in enumerate(self.shape):
             desc.shape[d] = e
-        desc.order = ref.order
+        desc.order = order
         desc.n_grids = len(self.names)
         desc.device = self.device
         h = ctypes.c_void_p()
@@ -146,18 +149,33 @@ class DeviceTarget:
         """Clear the whole buffer bound to ``name`` (async, on the domain's stream)."""
         L.call("stkb_zero", self.h, self.index[name])
 
-    def upload(self, name: str, data: np.ndarray, sync: bool = True) -> None:
+    def buffer_layout(self, name: str) -> tuple:
+        """(shape, order) of the grid whose buffer ``name`` is bound to now: swaps move
+        buffers, with their layouts, between names (executor.py:229-230)."""
+        b = ctypes.c_int32()
+        L.call("stkb_binding", self.h, self.index[name], ctypes.byref(b))
+        return self.layouts[self.names[b.value]] if b.value < len(self.names) else self.layouts[name]
+
+    def upload(self, name: str, data: np.ndarray, sync: bool = True, layout: Optional[tuple] = None) -> None:
         arr = self._host(data)
-        fn = "stkb_upload" if sync else "stkb_upload_async"
-        L.call(fn, self.h, self.index[name], arr.ctypes.data_as(ctypes.c_void_p))
+        shape, order = layout or self.buffer_layout(name)
+        if tuple(arr.shape) != tuple(e + 2 * order for e in shape):
+            raise ExecutionError(f"grid '{name}': host array {arr.shape} does not match shape {shape}/order {order}")
+        ext = (ctypes.c_int64 * 3)(*shape)
+        L.call("stkb_upload_grid", self.h, self.index[name], arr.ctypes.data_as(ctypes.c_void_p), ext, order,
+               int(bool(sync)))
         self._keep = arr
 
     def download(self, name: str, out: Optional[np.ndarray] = None, sync: bool = True) -> np.ndarray:
-        padded = tuple(e + 2 * self.order for e in self.shape)
+        shape, order = self.buffer_layout(name)
+        padded = tuple(e + 2 * order for e in shape)
         if out is None:
             out = np.empty(padded, dtype=self.np_dtype)
-        fn = "stkb_download" if sync else "stkb_download_async"
-        L.call(fn, self.h, self.index[name], out.ctypes.data_as(ctypes.c_void_p))
+        elif tuple(out.shape) != padded:
+            raise ExecutionError(f"grid '{name}': output array {out.shape} does not match {padded}")
+        ext = (ctypes.c_int64 * 3)(*shape)
+        L.call("stkb_download_grid", self.h, self.index[name], out.ctypes.data_as(ctypes.c_void_p), ext, order,
+               int(bool(sync)))
         return out
 
     def layout(self) -> dict:
@@ -181,7 +199,8 @@ class DeviceTarget:
     # -- program -----------------------------------------------------------------
     def compile_map(self, bmap, tag: int, box: Optional[tuple] = None) -> L.MapDesc:
         try:
-            plan = match_map(bmap, exact=self.precision == "exact")
+            # 1-D maps (gmem/smem/f4 plans, executor.py:543-549) run on the exact EXPR kernel
+            plan = match_map(bmap, exact=self.precision == "exact" or bmap.info.dims == 1)
         except MatchError as why:
             raise ExecutionError(f"kernel '{bmap.kernel.name}': {why}") from None
         self.plans.append(plan)
@@ -332,7 +351,7 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
         _host_swaps(bound.stmts, out, bindings or {})
         return out
     # grids no map touches still take part in swaps: give them device slots too
-    names = used + [n for n in grids if n not in used and _same_layout(grids[n], grids[used[0]])]
+    names = used + [n for n in grids if n not in used and _same_kind(grids[n], grids[used[0]])]
     out = {n: b.copy() for n, b in grids.items() if n not in names}
     dead = dead_on_entry(bound.stmts, names, bindings or {})
     h2d = d2h = 0
@@ -352,7 +371,7 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
         dt.sync()
         dt.execute(bound.stmts, bindings)
         for n in names:
-            b = grids[n]
+            b = grids[dt.names[dt_binding(dt, n)]] if dt_binding(dt, n) < len(dt.names) else grids[n]
             arr = _host_array(b.data.shape, dt.np_dtype, pinned)
             dt.download(n, arr, sync=False)
             d2h += arr.nbytes
@@ -378,7 +397,7 @@ _PARK_LOCK = threading.Lock()
 def _acquire(grids: dict, names: list, device, precision: str):
     dev = default_device() if device is None else device
     g0 = grids[names[0]]
-    key = (tuple(names), g0.dtype, tuple(g0.shape), g0.order, dev, precision)
+    key = (tuple(names), g0.dtype, tuple((tuple(grids[n].shape), grids[n].order) for n in names), dev, precision)
     with _PARK_LOCK:
         parked = _PARKED.pop(dev, None)
     if parked is not None:
@@ -431,7 +450,7 @@ def _reads_writes(bmap) -> tuple:
     params = dict(bmap.grid_args)
     reads, writes = set(), set()
     kern = bmap.kernel
-    from .program import walk, node_kind
+    from .front import walk, node_kind
 
     for e in [e for _, e in kern.locals] + [u.expr for u in kern.updates]:
         for n in walk(e):
@@ -510,8 +529,14 @@ def halo_is_zero(g) -> bool:
     return True
 
 
-def _same_layout(a, b) -> bool:
-    return (a.dtype, tuple(a.shape), a.order) == (b.dtype, tuple(b.shape), b.order)
+def _same_kind(a, b) -> bool:
+    return (a.dtype, len(a.shape)) == (b.dtype, len(b.shape))
+
+
+def dt_binding(dt, name: str) -> int:
+    b = ctypes.c_int32()
+    L.call("stkb_binding", dt.h, dt.index[name], ctypes.byref(b))
+    return b.value
 
 
 def _host_swaps(stmts, state: dict, bindings: dict) -> None:

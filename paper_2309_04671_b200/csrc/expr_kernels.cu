@@ -174,22 +174,32 @@ size_t compare_partial_bytes() { return sizeof(ComparePartial); }
 
 // copy `nrows` rows of `row_words` 32-bit words between two row pitches
 // (the unpitched GridBuffer layout <-> the 128-byte pitched device layout)
-__global__ void __launch_bounds__(256) repitch_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                                                      int64_t nrows, int64_t row_words, int64_t src_pitch,
-                                                      int64_t dst_pitch) {
-    for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-        const uint32_t* s = src + r * src_pitch;
-        uint32_t* d = dst + r * dst_pitch;
-        for (int64_t i = threadIdx.x; i < row_words; i += blockDim.x) d[i] = s[i];
+// rows [r0, r0 + nrows) of a host-layout box: row r is row r % rows_per_plane of plane
+// r / rows_per_plane; one side is the contiguous staging buffer (row r - r0 at
+// (r - r0) * row_words), the other the pitched device buffer (plane / row pitches)
+__global__ void __launch_bounds__(256) repitch_kernel(uint32_t* __restrict__ stage, uint32_t* __restrict__ dev,
+                                                      int64_t r0, int64_t nrows, int64_t rows_per_plane,
+                                                      int64_t row_words, int64_t row_pitch, int64_t plane_pitch,
+                                                      bool to_device) {
+    for (int64_t k = blockIdx.x; k < nrows; k += gridDim.x) {
+        const int64_t r = r0 + k;
+        uint32_t* s = stage + k * row_words;
+        uint32_t* d = dev + (r / rows_per_plane) * plane_pitch + (r % rows_per_plane) * row_pitch;
+        if (to_device)
+            for (int64_t i = threadIdx.x; i < row_words; i += blockDim.x) d[i] = s[i];
+        else
+            for (int64_t i = threadIdx.x; i < row_words; i += blockDim.x) s[i] = d[i];
     }
 }
 
-cudaError_t launch_repitch(const void* src, void* dst, int64_t nrows, int64_t row_bytes, int64_t src_pitch_bytes,
-                           int64_t dst_pitch_bytes, int num_sms, cudaStream_t s) {
+cudaError_t launch_repitch(void* stage, void* dev, int64_t r0, int64_t nrows, int64_t rows_per_plane,
+                           int64_t row_bytes, int64_t row_pitch_bytes, int64_t plane_pitch_bytes, bool to_device,
+                           int num_sms, cudaStream_t s) {
     if (nrows <= 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>(nrows, int64_t(num_sms) * 16);
-    repitch_kernel<<<int(blocks), 256, 0, s>>>(static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), nrows,
-                                               row_bytes / 4, src_pitch_bytes / 4, dst_pitch_bytes / 4);
+    repitch_kernel<<<int(blocks), 256, 0, s>>>(static_cast<uint32_t*>(stage), static_cast<uint32_t*>(dev), r0, nrows,
+                                               rows_per_plane, row_bytes / 4, row_pitch_bytes / 4,
+                                               plane_pitch_bytes / 4, to_device);
     return cudaGetLastError();
 }
 

@@ -28,8 +28,9 @@ cudaError_t launch_compare(int dtype, const Geometry& g, const void* ref, const 
                            int blocks, cudaStream_t s);
 size_t compare_partial_bytes();
 cudaError_t launch_signal_add(int32_t* p, int32_t v, cudaStream_t s);
-cudaError_t launch_repitch(const void* src, void* dst, int64_t nrows, int64_t row_bytes, int64_t src_pitch_bytes,
-                           int64_t dst_pitch_bytes, int num_sms, cudaStream_t s);
+cudaError_t launch_repitch(void* stage, void* dev, int64_t r0, int64_t nrows, int64_t rows_per_plane,
+                           int64_t row_bytes, int64_t row_pitch_bytes, int64_t plane_pitch_bytes, bool to_device,
+                           int num_sms, cudaStream_t s);
 struct Star2DArgs {
     int64_t pitch;
     int64_t lead;
@@ -605,7 +606,7 @@ int stkb_device_count(int32_t* count) {
 int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (!desc || !out) return fail(STKB_ERR_ARG, "null argument");
     if (desc->dtype != STKB_F32 && desc->dtype != STKB_F64) return fail(STKB_ERR_ARG, "dtype must be STKB_F32 or STKB_F64");
-    if (desc->ndim != 2 && desc->ndim != 3) return fail(STKB_ERR_UNSUPPORTED, "only 2-D and 3-D grids are supported");
+    if (desc->ndim < 1 || desc->ndim > 3) return fail(STKB_ERR_UNSUPPORTED, "grids have 1 to 3 dimensions");
     if (desc->n_grids < 1 || desc->n_grids > 32) return fail(STKB_ERR_ARG, "n_grids must be in 1..32");
     if (desc->order < 0 || desc->order > 16) return fail(STKB_ERR_ARG, "order must be in 0..16");
     for (int d = 0; d < desc->ndim; ++d)
@@ -619,8 +620,11 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (desc->ndim == 3) {
         g.n0 = desc->shape[0]; g.n1 = desc->shape[1]; g.n2 = desc->shape[2];
         g.order0 = desc->order;
-    } else {  // 2-D grids are lifted to a single d0 plane without d0 halo
+    } else if (desc->ndim == 2) {  // 2-D grids are lifted to a single d0 plane without d0 halo
         g.n0 = 1; g.n1 = desc->shape[0]; g.n2 = desc->shape[1];
+        g.order0 = 0;
+    } else {  // 1-D grids: one row of one plane (the d1 halo rows stay zero and unread)
+        g.n0 = 1; g.n1 = 1; g.n2 = desc->shape[0];
         g.order0 = 0;
     }
     g.order = desc->order;
@@ -748,52 +752,123 @@ static bool ensure_stage(stkb_domain* dom, size_t want) {
     return dom->d_stage != nullptr;
 }
 
-static int copy_h2d(stkb_domain* dom, int32_t name, const void* host) {
-    if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
-    if (int rc = check_name(dom, name, "stkb_upload")) return rc;
-    CUDA_TRY(cudaSetDevice(dom->desc.device));
-    mark_halo_dirty(dom, dom->binding[name]);
+// A host grid's C-order padded box in lifted 3-D terms: interior extents s and halo widths
+// h per axis (a 2-D grid is one plane without d0 halo, a 1-D grid one row of one plane).
+struct HostBox {
+    int64_t s[3];
+    int64_t h[3];
+    int64_t planes() const { return s[0] + 2 * h[0]; }
+    int64_t rows_per_plane() const { return s[1] + 2 * h[1]; }
+    int64_t row_elems() const { return s[2] + 2 * h[2]; }
+};
+
+static HostBox domain_box(const stkb_domain* dom) {
     const Geometry& g = dom->g;
-    const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
-    const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
-    char* dst = static_cast<char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
-    if (!ensure_stage(dom, rows * row)) {  // no memory for staging: direct pitched copy
-        CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(g.pitch) * dom->elem, host, row, row, rows, cudaMemcpyHostToDevice,
-                                   dom->stream));
+    HostBox b{{g.n0, g.n1, g.n2}, {g.order0, dom->desc.ndim >= 2 ? g.order : 0, g.order}};
+    return b;
+}
+
+// the layout of a grid of `shape` (ndim axes, as the domain) and halo `order`
+static int grid_box(const stkb_domain* dom, const int64_t* shape, int32_t order, HostBox* out) {
+    const int nd = dom->desc.ndim;
+    const Geometry& g = dom->g;
+    if (!shape) return fail(STKB_ERR_ARG, "null shape");
+    if (order < 0 || order > g.order) return fail(STKB_ERR_ARG, "grid order exceeds the domain's halo order");
+    HostBox b{{1, 1, 1}, {0, 0, 0}};
+    for (int d = 0; d < nd; ++d) {
+        b.s[3 - nd + d] = shape[d];
+        b.h[3 - nd + d] = order;
+    }
+    const int64_t ext[3] = {g.n0, g.n1, g.n2};
+    for (int d = 0; d < 3; ++d)
+        if (b.s[d] < 1 || b.s[d] > ext[d]) return fail(STKB_ERR_ARG, "grid extent exceeds the domain's");
+    *out = b;
+    return STKB_OK;
+}
+
+static bool same_box(const HostBox& a, const HostBox& b) {
+    for (int d = 0; d < 3; ++d)
+        if (a.s[d] != b.s[d] || a.h[d] != b.h[d]) return false;
+    return true;
+}
+
+// host box <-> pitched device buffer through the staging buffer: contiguous PCIe copies
+// of whole host rows, scattered/gathered on the device by the repitch kernel
+static int copy_box(stkb_domain* dom, int32_t name, const HostBox& hb, void* host, bool to_device) {
+    const Geometry& g = dom->g;
+    const size_t e = dom->elem;
+    const size_t row = size_t(hb.row_elems()) * e;
+    const int64_t rpp = hb.rows_per_plane();
+    const int64_t rows = hb.planes() * rpp;
+    char* base = static_cast<char*>(dom->bufs[dom->binding[name]]) + size_t(g.at(-hb.h[0], -hb.h[1], -hb.h[2])) * e;
+    const int64_t rp = g.pitch * int64_t(e), pp = g.plane * int64_t(e);
+    char* h = static_cast<char*>(host);
+    if (!ensure_stage(dom, size_t(rows) * row)) {  // no memory for staging: pitched copies, plane by plane
+        for (int64_t p = 0; p < hb.planes(); ++p) {
+            char* d = base + p * pp;
+            char* hp = h + size_t(p * rpp) * row;
+            if (to_device)
+                CUDA_TRY(cudaMemcpy2DAsync(d, size_t(rp), hp, row, row, size_t(rpp), cudaMemcpyHostToDevice, dom->stream));
+            else
+                CUDA_TRY(cudaMemcpy2DAsync(hp, row, d, size_t(rp), row, size_t(rpp), cudaMemcpyDeviceToHost, dom->stream));
+        }
         return STKB_OK;
     }
-    const size_t chunk_rows = std::max<size_t>(1, dom->stage_bytes / row);
-    const char* src = static_cast<const char*>(host);
-    for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
-        const size_t nr = std::min(chunk_rows, rows - r0);
-        CUDA_TRY(cudaMemcpyAsync(dom->d_stage, src + r0 * row, nr * row, cudaMemcpyHostToDevice, dom->stream));
-        CUDA_TRY(launch_repitch(dom->d_stage, dst + r0 * size_t(g.pitch) * dom->elem, int64_t(nr), int64_t(row),
-                                int64_t(row), int64_t(g.pitch) * int64_t(dom->elem), dom->num_sms, dom->stream));
+    const int64_t chunk = std::max<int64_t>(1, int64_t(dom->stage_bytes / row));
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+        const int64_t nr = std::min(chunk, rows - r0);
+        if (to_device) {
+            CUDA_TRY(cudaMemcpyAsync(dom->d_stage, h + size_t(r0) * row, size_t(nr) * row, cudaMemcpyHostToDevice,
+                                     dom->stream));
+            CUDA_TRY(launch_repitch(dom->d_stage, base, r0, nr, rpp, int64_t(row), rp, pp, true, dom->num_sms,
+                                    dom->stream));
+        } else {
+            CUDA_TRY(launch_repitch(dom->d_stage, base, r0, nr, rpp, int64_t(row), rp, pp, false, dom->num_sms,
+                                    dom->stream));
+            CUDA_TRY(cudaMemcpyAsync(h + size_t(r0) * row, dom->d_stage, size_t(nr) * row, cudaMemcpyDeviceToHost,
+                                     dom->stream));
+        }
     }
     return STKB_OK;
 }
 
-static int copy_d2h(stkb_domain* dom, int32_t name, void* host) {
+static int copy_h2d(stkb_domain* dom, int32_t name, const void* host, const HostBox* hb = nullptr) {
+    if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
+    if (int rc = check_name(dom, name, "stkb_upload")) return rc;
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    mark_halo_dirty(dom, dom->binding[name]);
+    const HostBox own = domain_box(dom);
+    if (hb && !same_box(*hb, own)) {  // a smaller box: every cell it does not cover is zero
+        const size_t bytes = size_t(dom->g.plane) * size_t(dom->g.n0 + 2 * dom->g.order0) * dom->elem;
+        CUDA_TRY(cudaMemsetAsync(dom->bufs[dom->binding[name]], 0, bytes, dom->stream));
+    }
+    return copy_box(dom, name, hb ? *hb : own, const_cast<void*>(host), true);
+}
+
+static int copy_d2h(stkb_domain* dom, int32_t name, void* host, const HostBox* hb = nullptr) {
     if (!dom || !host) return fail(STKB_ERR_ARG, "null argument");
     if (int rc = check_name(dom, name, "stkb_download")) return rc;
     CUDA_TRY(cudaSetDevice(dom->desc.device));
-    const Geometry& g = dom->g;
-    const size_t row = size_t(g.n2 + 2 * g.order) * dom->elem;
-    const size_t rows = size_t(g.n0 + 2 * g.order0) * size_t(g.n1 + 2 * g.order);
-    const char* src = static_cast<const char*>(dom->bufs[dom->binding[name]]) + (g.lead - g.order) * dom->elem;
-    if (!ensure_stage(dom, rows * row)) {
-        CUDA_TRY(cudaMemcpy2DAsync(host, row, src, size_t(g.pitch) * dom->elem, row, rows, cudaMemcpyDeviceToHost,
-                                   dom->stream));
-        return STKB_OK;
-    }
-    const size_t chunk_rows = std::max<size_t>(1, dom->stage_bytes / row);
-    char* out = static_cast<char*>(host);
-    for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
-        const size_t nr = std::min(chunk_rows, rows - r0);
-        CUDA_TRY(launch_repitch(src + r0 * size_t(g.pitch) * dom->elem, dom->d_stage, int64_t(nr), int64_t(row),
-                                int64_t(g.pitch) * int64_t(dom->elem), int64_t(row), dom->num_sms, dom->stream));
-        CUDA_TRY(cudaMemcpyAsync(out + r0 * row, dom->d_stage, nr * row, cudaMemcpyDeviceToHost, dom->stream));
-    }
+    return copy_box(dom, name, hb ? *hb : domain_box(dom), host, false);
+}
+
+int stkb_upload_grid(stkb_domain* dom, int32_t name, const void* host, const int64_t* shape, int32_t order,
+                     int32_t sync) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    HostBox hb;
+    if (int rc = grid_box(dom, shape, order, &hb)) return rc;
+    if (int rc = copy_h2d(dom, name, host, &hb)) return rc;
+    if (sync) CUDA_TRY(cudaStreamSynchronize(dom->stream));
+    return STKB_OK;
+}
+
+int stkb_download_grid(stkb_domain* dom, int32_t name, void* host, const int64_t* shape, int32_t order,
+                       int32_t sync) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    HostBox hb;
+    if (int rc = grid_box(dom, shape, order, &hb)) return rc;
+    if (int rc = copy_d2h(dom, name, host, &hb)) return rc;
+    if (sync) CUDA_TRY(cudaStreamSynchronize(dom->stream));
     return STKB_OK;
 }
 
@@ -835,10 +910,14 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     int64_t lo[3], hi[3];
     if (nd == 3) {
         for (int i = 0; i < 3; ++i) { lo[i] = d.lo[i]; hi[i] = d.hi[i]; }
-    } else {
+    } else if (nd == 2) {
         lo[0] = 0; hi[0] = 1;
         lo[1] = d.lo[0]; hi[1] = d.hi[0];
         lo[2] = d.lo[1]; hi[2] = d.hi[1];
+    } else {
+        lo[0] = 0; hi[0] = 1;
+        lo[1] = 0; hi[1] = 1;
+        lo[2] = d.lo[0]; hi[2] = d.hi[0];
     }
     const int64_t ext[3] = {g.n0, g.n1, g.n2};
     for (int i = 0; i < 3; ++i)
@@ -849,7 +928,7 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
     if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX) {
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
-            return fail(STKB_ERR_UNSUPPORTED, "2-D grids stream star and box maps only");
+            return fail(STKB_ERR_UNSUPPORTED, nd == 1 ? "1-D maps run as EXPR maps" : "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
         if (d.kind == STKB_MAP_BOX && nd == 3) {
             const int n = 2 * d.radius + 1;
@@ -884,6 +963,7 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
             const int32_t* ins = &op.code[5 * pc];
             int32_t oz = ins[2], oy = ins[3], ox = ins[4];
             if (nd == 2 && (ins[0] == STKB_OP_READ || ins[0] == STKB_OP_STORE)) { ox = ins[3]; oy = ins[2]; oz = 0; }
+            if (nd == 1 && (ins[0] == STKB_OP_READ || ins[0] == STKB_OP_STORE)) { ox = ins[2]; oy = 0; oz = 0; }
             switch (ins[0]) {
                 case STKB_OP_CONST:
                     if (ins[1] < 0 || ins[1] >= d.n_consts) return fail(STKB_ERR_ARG, "EXPR: const index");

@@ -21,7 +21,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Optional
 
-from .program import node_kind
+from .front import node_kind
 
 MAX_FAST_RADIUS = 4
 MAX_BOX_RADIUS = 4

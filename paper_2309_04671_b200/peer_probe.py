@@ -30,7 +30,9 @@ def run(dev_a: int, dev_b: int, steps: int = 3) -> dict:
 
     from . import corpus
     from .backend import DeviceTarget
-    from .grids import GridBuffer, fill_loguniform
+    from .front import module
+
+    GridBuffer, fill_loguniform = module("grids").GridBuffer, module("grids").fill_loguniform
     from .slabs import DeviceSlabEngine, SlabPlan, connect_local
 
     shape = (24, 40, 136)

@@ -28,7 +28,7 @@ from typing import Optional
 
 import numpy as np
 
-from .program import node_kind, stmt_kind, walk
+from .front import node_kind, stmt_kind, walk
 
 
 def partition(n0: int, world: int) -> list:
@@ -159,7 +159,7 @@ def exchange(dist, plan: SlabPlan, views: dict, group=None):
 def localize(body: tuple, start: int, size: int) -> tuple:
     """The step body as seen by the slab [start, start+size): every map's
     regions are clipped to the slab and shifted to local d0 coordinates."""
-    from .program import BoundMap, Region
+    import dataclasses
 
     out = []
     for s in body:
@@ -171,8 +171,8 @@ def localize(body: tuple, start: int, size: int) -> tuple:
             (lo, hi), rest = r.bounds[0], tuple(r.bounds[1:])
             lo, hi = max(lo, start), min(hi, start + size)
             if hi > lo:
-                regs.append(Region(((lo - start, hi - start),) + rest, r.tag))
-        out.append(BoundMap(s.kernel, s.info, tuple(s.grid_args), tuple(s.scalar_args), s.spec, tuple(regs)))
+                regs.append(dataclasses.replace(r, bounds=((lo - start, hi - start),) + rest))
+        out.append(dataclasses.replace(s, regions=tuple(regs)))
     return tuple(out)
 
 
@@ -259,7 +259,9 @@ class DeviceSlabEngine:
         import torch
 
         from .backend import DeviceTarget
-        from .grids import GridBuffer
+        from .front import module
+
+        GridBuffer = module("grids").GridBuffer
 
         self.torch = torch
         self.plan = plan
@@ -651,8 +653,10 @@ def slab_e2e(builder: str, shape, dtype: str, k: int, slab: SlabPlan, dist, devi
     import torch
 
     from . import corpus
-    from .grids import GridBuffer
-    from .planning import plan_gpu
+    from .front import module
+
+    GridBuffer = module("grids").GridBuffer
+    plan_gpu = module("planning").plan_gpu
 
     bound, decls = corpus.config_target(builder, shape, k, dtype)
     local_shape = (slab.size,) + tuple(shape[1:])

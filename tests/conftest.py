@@ -14,7 +14,7 @@ GOLDEN = ROOT / "tests" / "golden"
 sys.path.insert(0, str(ROOT))
 
 from paper_2309_04671_b200 import corpus  # noqa: E402
-from paper_2309_04671_b200.grids import GridBuffer  # noqa: E402
+from paper_2309_04671_b200 import GridBuffer  # noqa: E402
 
 
 def pytest_configure(config):
@@ -50,9 +50,10 @@ def _order(meta) -> int:
 
 
 def build_case(meta):
-    """This package's own BoundTarget for a golden case (no reference needed)."""
-    return corpus.config_target(meta["builder"], tuple(meta["shape"]), meta["iters"], meta["dtype"],
-                                meta["map_width"], meta["scheme"])[0]
+    """The reference-bound BoundTarget of a golden case: the very program text the
+    reference ran to make the fixture, parsed and bound by the reference front end."""
+    z = np.load(GOLDEN / f"{meta['case']}.npz")
+    return corpus.bind_text(str(z["source"]), meta["iters"], meta["scheme"], f"{meta['case']}.stpy")[0]
 
 
 def gpu_available() -> bool:

@@ -19,8 +19,8 @@ def main():
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2309_04671_b200 import corpus
-    from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
-    from paper_2309_04671_b200.planning import plan_gpu
+    from paper_2309_04671_b200 import GridBuffer, fill_loguniform
+    from paper_2309_04671_b200 import plan_gpu
     from paper_2309_04671_b200.slabs import SlabPlan, run_slab
 
     dist.init_process_group("gloo")

@@ -11,7 +11,7 @@ import pytest
 from oracle import oracle
 from paper_2309_04671_b200 import _lib as L
 from paper_2309_04671_b200 import compare, corpus
-from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
+from paper_2309_04671_b200 import GridBuffer, fill_loguniform
 from paper_2309_04671_b200.matcher import coef_index
 
 pytestmark = pytest.mark.gpu

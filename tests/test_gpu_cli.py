@@ -11,7 +11,7 @@ import pytest
 from conftest import ROOT, build_case, load_golden
 from oracle import oracle
 from paper_2309_04671_b200 import compare
-from paper_2309_04671_b200.grids import load_grid, save_grid
+from paper_2309_04671_b200 import load_grid, save_grid
 
 pytestmark = pytest.mark.gpu
 
@@ -41,6 +41,7 @@ def test_cli_reports_bad_plan_as_exit_1(tmp_path):
     _, source, _, _, _ = load_golden("star3d4r_16")
     prog = tmp_path / "p.stpy"
     prog.write_text(source)
-    r = subprocess.run([sys.executable, "-m", "paper_2309_04671_b200", "run", str(prog), "--template", "tma",
+    r = subprocess.run([sys.executable, "-m", "paper_2309_04671_b200", "run", str(prog), "--backend", "gpu",
+                        "--template", "tma",
                         "-o", str(tmp_path / "o")], cwd=ROOT, capture_output=True, text=True)
     assert r.returncode == 1 and "unknown GPU template" in r.stderr

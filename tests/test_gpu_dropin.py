@@ -1,0 +1,322 @@
+"""The drop-in, run INSIDE the reference — B200 only.
+
+`integrate.install()` patches the reference's own ``stencilkit.executor.run_tile_plan``
+(the INTEGRATION.md change, applied at run time) and these tests then drive the
+reference's public API — its ``SourceUnit``s from ``stencilkit.corpus.source_text``,
+its ``plan_gpu`` plans, its ``GridBuffer``s, its ``run_target`` oracle and its CLI —
+exactly as the reference's own tests do:
+
+* tests/test_executor.py:228-302 (tile plans: gmem/shift/f4, all six templates,
+  prefetch/async invariance, the dimension-mismatch error), restated;
+* tests/test_acceptance.py:155-190 (criterion 6: every table kernel x GPU template
+  within 1e-7 max / 1e-8 RMSD relative), restated;
+* cli.py:246-283 ``run --backend gpu --oracle`` through the reference's ``cli.main``.
+
+Precision: the patch's default is ``exact`` (float64 in parse order, one rounding:
+the reference's own bar, ``array_equal`` / 1e-7 / 1e-8, holds); the tuned ``fast``
+path is held to the north-star tolerance (fp32 max relative error <= 1e-5).
+"""
+
+from __future__ import annotations
+
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2309_04671_b200 import front, integrate
+
+pytestmark = pytest.mark.gpu
+
+sk_corpus = front.module("corpus")
+sk_executor = front.module("executor")
+sk_grids = front.module("grids")
+sk_parser = front.module("parser")
+sk_planning = front.module("planning")
+sk_analysis = front.module("analysis")
+
+FAST_TOL = {"f32": 1e-5, "f64": 1e-12}
+MAX_TOL, RMSD_TOL = 1e-7, 1e-8  # test_acceptance.py MAX_TOL / RMSD_TOL, cli.py:37-38
+
+
+# -- the reference's conftest helpers (tests/conftest.py:11-33), on its API ----------------
+def make_unit(name, shape=None, iters=3, **kwargs):
+    text = sk_corpus.source_text(name, shape=shape, iters=iters, **kwargs)
+    unit = sk_parser.parse_source(text, f"{name}.stpy")
+    assert not sk_parser.validate(unit)
+    return unit
+
+
+def make_grids(unit, seed=7):
+    grids = {g.name: sk_grids.GridBuffer.zeros(g.shape, g.order, g.dtype) for g in unit.grids}
+    first = unit.launch.args[0] if unit.launch else unit.grids[0].name
+    sk_grids.fill_loguniform(grids[first], seed)
+    return grids
+
+
+def kernel_info(unit):
+    kernel = unit.kernels[0]
+    grid_params = [n for n, t in kernel.params if t == "grid"]
+    return sk_analysis.analyze_kernel(kernel, {p: g for p, g in zip(grid_params, unit.grids)})
+
+
+@pytest.fixture(params=["exact", "fast"])
+def patched(request):
+    """run_tile_plan with the B200 GPU branch installed, in one precision."""
+    integrate.install(request.param)
+    yield request.param
+    integrate.uninstall()
+
+
+def run_tile_plan(*a, **k):
+    return sk_executor.run_tile_plan(*a, **k)  # looked up at call time: the patched one
+
+
+def check(ref, out, precision, exact_bitwise=False):
+    rep = sk_grids.compare(ref, out)
+    if precision == "exact":
+        if exact_bitwise:
+            assert np.array_equal(ref.data, out.data)
+        assert rep.max_relative <= MAX_TOL and rep.rmsd_relative <= RMSD_TOL, rep.render()
+    else:
+        assert rep.max_relative <= FAST_TOL[ref.dtype], rep.render()
+    return rep
+
+
+# -- tests/test_executor.py:228-302, through the patched run_tile_plan ------------------------
+def test_patch_routes_gpu_plans_only(patched):
+    assert integrate.installed()
+    unit = make_unit("star3d2r", shape=(12, 12, 12), iters=2)
+    grids = make_grids(unit, seed=35)
+    ref = sk_executor.run_target(unit, grids)
+    omp = run_tile_plan(unit, sk_planning.plan_omp(kernel_info(unit), {"template": "loop"}), grids)
+    assert np.array_equal(ref["u"].data, omp["u"].data)  # OmpPlan: the reference's own emulation
+    from paper_2309_04671_b200.backend import LAST_RUN
+
+    LAST_RUN.clear()
+    run_tile_plan(unit, sk_planning.plan_gpu(kernel_info(unit), {"template": "unroll"}), grids)
+    assert LAST_RUN.get("launches", 0) >= 1  # GpuPlan: the device
+
+
+def test_gmem_exact_on_star3d2r(patched):
+    unit = make_unit("star3d2r", shape=(16, 16, 16), iters=2)
+    grids = make_grids(unit, seed=21)
+    ref = sk_executor.run_target(unit, grids)
+    plan = sk_planning.plan_gpu(kernel_info(unit), {"template": "gmem", "threadsPerBlock": (8, 8, 8)})
+    out = run_tile_plan(unit, plan, grids)
+    check(ref["u"], out["u"], patched, exact_bitwise=True)
+
+
+def test_shift_on_box3d2r_within_tolerance(patched):
+    unit = make_unit("box3d2r", shape=(20, 20, 20), iters=2)
+    grids = make_grids(unit, seed=22)
+    ref = sk_executor.run_target(unit, grids)
+    plan = sk_planning.plan_gpu(kernel_info(unit), {"template": "shift", "planeDims": (16, 16)})
+    check(ref["u"], run_tile_plan(unit, plan, grids)["u"], patched)
+
+
+def test_f4_exact_on_star2d4r(patched):
+    unit = make_unit("star2d4r", shape=(16, 16), iters=2)
+    grids = make_grids(unit, seed=23)
+    ref = sk_executor.run_target(unit, grids)
+    out = run_tile_plan(unit, sk_planning.plan_gpu(kernel_info(unit), {"template": "f4"}), grids)
+    check(ref["u"], out["u"], patched, exact_bitwise=True)
+
+
+@pytest.mark.parametrize("template", ["gmem", "smem", "f4", "shift", "unroll", "semi"])
+def test_all_templates_on_star3d2r(patched, template):
+    unit = make_unit("star3d2r", shape=(12, 12, 12), iters=2)
+    grids = make_grids(unit, seed=31)
+    ref = sk_executor.run_target(unit, grids)
+    plan = sk_planning.plan_gpu(kernel_info(unit), {"template": template, "threadsPerBlock": (4, 4, 4)})
+    check(ref["u"], run_tile_plan(unit, plan, grids)["u"], patched)
+
+
+def test_prefetch_and_async_do_not_change_numbers(patched):
+    unit = make_unit("box3d2r", shape=(12, 12, 12), iters=2)
+    grids = make_grids(unit, seed=33)
+    info = kernel_info(unit)
+    base = run_tile_plan(unit, sk_planning.plan_gpu(info, {"template": "unroll"}), grids)
+    for extra in ({"prefetch": True}, {"asyncMemcpy": True, "computeCapability": "10.0"},
+                  {"prefetch": True, "asyncMemcpy": True, "computeCapability": "8.0"}):
+        out = run_tile_plan(unit, sk_planning.plan_gpu(info, {"template": "unroll", **extra}), grids)
+        assert np.array_equal(base["u"].data, out["u"].data)
+
+
+def test_plan_dimension_mismatch_rejected(patched):
+    unit2d = make_unit("star2d1r", shape=(8, 8), iters=1)
+    plan3d = sk_planning.plan_gpu(kernel_info(make_unit("star3d1r")), {"template": "gmem"})
+    with pytest.raises(sk_executor.ExecutionError, match="plan is 3D"):
+        run_tile_plan(unit2d, plan3d, make_grids(unit2d))
+
+
+def test_semi_rejects_box_stencils(patched):
+    """The planner refuses semi for a box (planning.py:155-157); a hand-made semi plan
+    reaching the executor is refused there (executor.py:540-541)."""
+    import dataclasses
+
+    unit = make_unit("box3d1r", shape=(8, 8, 8), iters=1)
+    with pytest.raises(sk_planning.PlanError, match="star-shaped"):
+        sk_planning.plan_gpu(kernel_info(unit), {"template": "semi"})
+    plan = dataclasses.replace(sk_planning.plan_gpu(kernel_info(unit), {"template": "unroll"}), template="semi")
+    with pytest.raises(sk_executor.ExecutionError, match="star-shaped"):
+        run_tile_plan(unit, plan, make_grids(unit))
+
+
+# -- tests/test_acceptance.py:155-190 (criterion 6), GPU combinations ------------------------
+def _gpu_combinations():
+    for kernel in sk_corpus.TABLE_KERNELS:
+        shape = (64, 64) if kernel.dims == 2 else (16, 16, 16)
+        templates = ["gmem", "smem", "f4", "shift", "unroll"] + (["semi"] if kernel.shape == "star" else [])
+        for template in templates:
+            yield kernel.name, shape, template
+
+
+COMBOS = list(_gpu_combinations())
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_criterion_6_gpu_accuracy_suite(precision):
+    integrate.install(precision)
+    try:
+        worst = 0.0
+        for i, (name, shape, template) in enumerate(COMBOS):
+            unit = make_unit(name, shape=shape, iters=3)
+            grids = make_grids(unit, seed=1000 + i)
+            reference = sk_executor.run_target(unit, grids)
+            plan = sk_planning.plan_gpu(kernel_info(unit), {"template": template, "threadsPerBlock": (8, 4, 4)})
+            result = run_tile_plan(unit, plan, grids)
+            rep = sk_grids.compare(reference["u"], result["u"])
+            if precision == "exact":
+                assert rep.max_relative <= MAX_TOL and rep.rmsd_relative <= RMSD_TOL, (name, template, rep.render())
+            else:
+                assert rep.max_relative <= FAST_TOL["f32"], (name, template, rep.render())
+            worst = max(worst, rep.max_relative)
+        assert len(COMBOS) >= 100
+    finally:
+        integrate.uninstall()
+
+
+# -- the reference CLI (cli.py:246-283) with the drop-in installed ----------------------------
+@pytest.mark.parametrize("name,precision,tol", [("star3d4r", "fast", "1e-5"), ("star3d2r", "exact", None),
+                                                ("j3d27pt", "exact", None), ("star2d4r", "fast", "1e-5")])
+def test_reference_cli_run_gpu_oracle(tmp_path, name, precision, tol):
+    shape = (16, 16) if name.startswith("star2d") else (20, 18, 24)
+    prog = tmp_path / f"{name}.stpy"
+    prog.write_text(sk_corpus.source_text(name, shape=shape, iters=4))
+    cmd = [sys.executable, "-m", "paper_2309_04671_b200", "run", str(prog), "--backend", "gpu", "--template",
+           "unroll" if name != "star2d4r" else "shift", "--capability", "10.0", "--random-init", "7", "--oracle",
+           "--precision", precision, "-o", str(tmp_path / "out"), "--profile"]
+    if tol:  # the north-star tolerance for the fast path, on both of the CLI's measures
+        cmd += ["--max-tol", tol, "--rmsd-tol", tol]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "max=" in r.stdout and "execution=" in r.stdout
+    assert (tmp_path / "out" / "u.grid").exists() and (tmp_path / "out" / "v.grid").exists()
+
+
+def test_reference_cli_tolerance_failure_is_exit_2(tmp_path):
+    """fast fp32 cannot meet 1e-12: the reference CLI's exit code 2 (cli.py:281-283)."""
+    prog = tmp_path / "p.stpy"
+    prog.write_text(sk_corpus.source_text("star3d4r", shape=(16, 16, 16), iters=3))
+    r = subprocess.run([sys.executable, "-m", "paper_2309_04671_b200", "run", str(prog), "--backend", "gpu",
+                        "--capability", "10.0", "--random-init", "3", "--oracle", "--max-tol", "1e-12",
+                        "--precision", "fast", "-o", str(tmp_path / "o")], cwd=ROOT, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 2, r.stdout + r.stderr
+
+
+# -- programs the reference accepts with grids of different layouts / rank 1 ----------------
+def _wave_text(shape, iters, kap_decl):
+    from paper_2309_04671_b200 import corpus
+
+    text = corpus.program_text("wave", shape, iters)
+    old = f"kap = st.grid(dtype=st.f32, shape=({', '.join(map(str, shape))}), order=4)"
+    assert old in text
+    return text.replace(old, kap_decl)
+
+
+@pytest.mark.parametrize("kap_decl", ["kap = st.grid(dtype=st.f32, shape=(24, 20, 36), order=0)",
+                                      "kap = st.grid(dtype=st.f32, shape=(26, 23, 40), order=1)",
+                                      "kap = st.grid(dtype=st.f32, shape=(24, 20, 36), order=2)"])
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_wave_with_kappa_in_its_own_layout(kap_decl, precision):
+    """parser.py:681-691 checks each grid's order against its own reads only: a
+    centre-only kappa may have order 0 (or another shape); the device domain takes
+    the largest geometry and every grid keeps its own host layout."""
+    from paper_2309_04671_b200 import corpus, run_gpu
+
+    shape = (24, 20, 36)
+    bound, decls = corpus.bind_text(_wave_text(shape, 5, kap_decl), 5)
+    grids = corpus.grids_for(decls)
+    sk_grids.fill_loguniform(grids["u"], 3)
+    grids["up"].data[...] = grids["u"].data
+    grids["kap"].interior[...] = np.float32(0.01)
+    ref = sk_executor.run_target(bound, grids)
+    plan = sk_planning.plan_gpu(bound.stmts[0].body[0].info, {"template": "unroll", "computeCapability": "10.0"})
+    got = run_gpu(bound, plan, grids, precision=precision)
+    for n in ref:
+        assert got[n].data.shape == ref[n].data.shape and got[n].order == ref[n].order, n
+        if precision == "exact":
+            assert np.array_equal(got[n].data, ref[n].data), n
+        else:
+            assert sk_grids.compare(ref[n], got[n]).max_relative <= 1e-5, n
+
+
+def test_swaps_move_layouts_with_buffers():
+    """Grids of different orders swapped every step: each name ends up holding the other
+    grid's buffer, with that buffer's layout (executor.py:229-230)."""
+    from paper_2309_04671_b200 import corpus, run_gpu
+
+    text = sk_corpus.source_text("star3d1r", shape=(10, 12, 14), iters=3)
+    text = text.replace("v = st.grid(dtype=st.f32, shape=(10, 12, 14), order=1)",
+                        "v = st.grid(dtype=st.f32, shape=(10, 12, 14), order=3)")
+    bound, decls = corpus.bind_text(text, 3)
+    grids = corpus.grids_for(decls)
+    sk_grids.fill_loguniform(grids["u"], 9)
+    ref = sk_executor.run_target(bound, grids)
+    plan = sk_planning.plan_gpu(bound.stmts[0].body[0].info, {"template": "gmem"})
+    got = run_gpu(bound, plan, grids, precision="exact")
+    for n in ref:
+        assert got[n].order == ref[n].order and np.array_equal(got[n].data, ref[n].data), n
+
+
+ONE_D = """import stencilpy as st
+
+@st.kernel
+def kernel_smooth1d(u: st.grid, v: st.grid):
+    v.at(0).set(0.25 * u.at(-2) + 0.5 * u.at(0) + 0.125 * u.at(1) + 0.125 * u.at(2))
+
+@st.target
+def target_smooth1d(u: st.grid, v: st.grid, iter: st.i32):
+    for _t in range(iter):
+        st.map(e=u.shape)(kernel_smooth1d)(u, v)
+        (v, u) = (u, v)
+
+u = st.grid(dtype=st.f64, shape=(1000,), order=2)
+v = st.grid(dtype=st.f64, shape=(1000,), order=2)
+st.launch(
+    backend=st.seq()
+)(target_smooth1d)(u, v, 7)
+"""
+
+
+@pytest.mark.parametrize("template", ["gmem", "smem", "f4"])
+def test_one_d_maps(template):
+    """1-D maps are accepted by gmem/smem/f4 plans (planning.py:84-85, executor.py:543-549):
+    they run on the exact EXPR kernel (bit-identical); streaming templates are refused
+    with the reference's message."""
+    from paper_2309_04671_b200 import corpus, run_gpu
+
+    bound, decls = corpus.bind_text(ONE_D, 7)
+    grids = corpus.grids_for(decls)
+    sk_grids.fill_loguniform(grids["u"], 4)
+    ref = sk_executor.run_target(bound, grids)
+    info = bound.stmts[0].body[0].info
+    got = run_gpu(bound, sk_planning.plan_gpu(info, {"template": template}), grids)
+    for n in ref:
+        assert np.array_equal(got[n].data, ref[n].data), n
+    with pytest.raises(sk_executor.ExecutionError, match="2D or 3D"):
+        run_gpu(bound, sk_planning.plan_gpu(info, {"template": "unroll"}), grids)

@@ -17,8 +17,8 @@ from conftest import build_case, golden_cases, load_golden
 from oracle import oracle
 from paper_2309_04671_b200 import DeviceTarget, ExecutionError, compare, fill_loguniform, run_gpu
 from paper_2309_04671_b200 import corpus
-from paper_2309_04671_b200.grids import GridBuffer
-from paper_2309_04671_b200.planning import plan_gpu
+from paper_2309_04671_b200 import GridBuffer
+from paper_2309_04671_b200 import plan_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -209,7 +209,11 @@ def test_scaling_by_two_is_exact_at_full_size():
     import torch
 
     from paper_2309_04671_b200 import _lib as L
-    from paper_2309_04671_b200.program import BoundMap, BoundSwap
+    import dataclasses
+
+    from paper_2309_04671_b200.front import module
+
+    BoundSwap = module("analysis").BoundSwap
 
     shape = (1024, 1024, 1024)
     bound, _ = corpus.config_target("star3d4r_norm", shape, 3)
@@ -224,7 +228,7 @@ def test_scaling_by_two_is_exact_at_full_size():
         del vals
         torch.cuda.synchronize()
         bmap = next(_maps(bound.stmts))
-        m2 = BoundMap(bmap.kernel, bmap.info, (("u", "u2"), ("v", "v2")), (), bmap.spec, bmap.regions)
+        m2 = dataclasses.replace(bmap, grid_args=(("u", "u2"), ("v", "v2")), scalar_args=())
         dt.set_program((bmap, m2, BoundSwap("v", "u"), BoundSwap("v2", "u2")))
         dt.run(3)
         dt.sync()
@@ -267,7 +271,7 @@ def test_fast_vs_exact_one_step_at_full_size(builder):
     import torch
 
     from paper_2309_04671_b200 import _lib as L
-    from paper_2309_04671_b200.program import BoundMap
+    import dataclasses
 
     shape = (1024, 1024, 1024)
     bound, decls = corpus.config_target(builder, shape, 1)
@@ -296,7 +300,7 @@ def test_fast_vs_exact_one_step_at_full_size(builder):
         if builder == "wave":
             # exact reads up (prev) from the extra copy, i.e. the pre-step values
             args = tuple((p, extra if p in ("up",) else g) for p, g in bmap.grid_args)
-        m2 = BoundMap(bmap.kernel, bmap.info, args, bmap.scalar_args, bmap.spec, bmap.regions)
+        m2 = dataclasses.replace(bmap, grid_args=args)
         exact_plan = __import__("paper_2309_04671_b200.matcher", fromlist=["compile_expr"]).compile_expr(m2)
         exact_plan.box = ((0, 1024),) * 3
         d = fast.map_desc(exact_plan, 1)

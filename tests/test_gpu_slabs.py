@@ -20,7 +20,7 @@ import pytest
 
 from oracle import oracle
 from paper_2309_04671_b200 import compare, corpus
-from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
+from paper_2309_04671_b200 import GridBuffer, fill_loguniform
 from paper_2309_04671_b200.slabs import DeviceSlabEngine, SlabPlan
 
 pytestmark = pytest.mark.gpu
@@ -157,7 +157,7 @@ def test_device_slabs_match_unsplit_oracle(case, transport):
 
 def test_run_slab_single_rank_matches_run_gpu():
     from paper_2309_04671_b200 import run_gpu
-    from paper_2309_04671_b200.planning import plan_gpu
+    from paper_2309_04671_b200 import plan_gpu
     from paper_2309_04671_b200.slabs import run_slab
 
     bound, decls, grids = _case("star3d4r_norm", (36, 40, 72), 5)

@@ -16,8 +16,8 @@ import pytest
 from oracle import oracle
 from paper_2309_04671_b200 import DeviceTarget, compare, corpus, fill_loguniform, run_gpu
 from paper_2309_04671_b200 import _lib as L
-from paper_2309_04671_b200.grids import GridBuffer
-from paper_2309_04671_b200.planning import plan_gpu
+from paper_2309_04671_b200 import GridBuffer
+from paper_2309_04671_b200 import plan_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -162,3 +162,55 @@ def test_fused_repeated_runs_and_scratch_reuse():
     for k in range(2):
         for n in ("u", "v"):
             assert np.array_equal(res[False][k][n], res[True][k][n]), (k, n)
+
+
+BC_TEXT = """import stencilpy as st
+
+@st.kernel
+def kernel_bc(u: st.grid, v: st.grid):
+    u.at(0, 0, 0).set(0.5 * v.at(0, 0, 0) + 0.25)
+
+@st.target
+def target_bc(u: st.grid, v: st.grid):
+    st.map(e=u.shape)(kernel_bc)(u, v)
+
+u = st.grid(dtype=st.f32, shape=({shape}), order=1)
+v = st.grid(dtype=st.f32, shape=({shape}), order=1)
+st.launch(
+    backend=st.seq()
+)(target_bc)(u, v)
+"""
+
+
+@pytest.mark.parametrize("steps", [6, 7])
+def test_fused_pair_invalidated_by_writes_outside_the_box(steps):
+    """`for k: { loop(v = S(u) on a sub-box; swap); bc(u) over the whole interior }`:
+    the map between the loops rewrites u outside the fused map's box, so the fused
+    sweeps' scratch must take u over again (a stale scratch would feed old values
+    outside the box to the second sweep as neighbours).  Fused == single steps."""
+    shape = (20, 24, 70)
+    box = ((3, 17), (4, 20), (9, 60))
+    bound, grids = _inputs("star3d1r", shape, "f32", steps)
+    bc_bound, _ = corpus.bind_text(BC_TEXT.format(shape=", ".join(map(str, shape))))
+    bc = bc_bound.stmts[0]
+    body = next(s for s in bound.stmts if type(s).__name__ == "BoundFor").body
+    bmap = next(s for s in body if type(s).__name__ == "BoundMap")
+    res = {}
+    for fused in (False, True):
+        with DeviceTarget(grids, ["u", "v"]) as dt:
+            for n in ("u", "v"):
+                dt.upload(n, grids[n].data)
+            dt.set_fused_steps(fused)
+            for _ in range(3):
+                d = dt.compile_map(bmap, 0, box=box)
+                L.call("stkb_program_reset", dt.h)
+                L.call("stkb_program_add_map", dt.h, ctypes.byref(d))
+                L.call("stkb_program_add_swap", dt.h, dt.index["v"], dt.index["u"])
+                dt._program_key = None
+                dt.run(steps)
+                dt.set_program((bc,))
+                dt.run(1)
+            dt.sync()
+            res[fused] = {n: dt.download(n) for n in ("u", "v")}
+    for n in ("u", "v"):
+        assert np.array_equal(res[False][n], res[True][n]), n

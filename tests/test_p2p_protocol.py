@@ -28,7 +28,7 @@ from types import SimpleNamespace
 import pytest
 
 from paper_2309_04671_b200 import _lib, corpus
-from paper_2309_04671_b200.program import stmt_kind
+from paper_2309_04671_b200.front import stmt_kind
 from paper_2309_04671_b200.slabs import (DeviceSlabEngine, SlabPlan, d0_read_reach, exchange_schedule,
                                          run_step_p2p, written)
 

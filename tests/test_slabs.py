@@ -22,7 +22,7 @@ import torch.multiprocessing as mp
 
 from oracle import oracle
 from paper_2309_04671_b200 import corpus
-from paper_2309_04671_b200.grids import GridBuffer, fill_loguniform
+from paper_2309_04671_b200 import GridBuffer, fill_loguniform
 from paper_2309_04671_b200.slabs import SlabPlan, exchange_schedule, localize, partition, run_step
 
 

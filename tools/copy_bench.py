@@ -11,7 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2309_04671_b200 import DeviceTarget  # noqa: E402
-from paper_2309_04671_b200.grids import GridBuffer  # noqa: E402
+from paper_2309_04671_b200 import GridBuffer  # noqa: E402
 
 shape, o = (1024, 1024, 1024), 4
 padded = tuple(e + 2 * o for e in shape)

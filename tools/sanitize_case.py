@@ -9,8 +9,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 from paper_2309_04671_b200 import corpus, fill_loguniform, run_gpu  # noqa: E402
-from paper_2309_04671_b200.grids import GridBuffer  # noqa: E402
-from paper_2309_04671_b200.planning import plan_gpu  # noqa: E402
+from paper_2309_04671_b200 import GridBuffer  # noqa: E402
+from paper_2309_04671_b200 import plan_gpu  # noqa: E402
 
 
 def run(builder, shape, steps, precision="fast"):

@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2309_04671_b200 import DeviceTarget  # noqa: E402
-from paper_2309_04671_b200.grids import GridBuffer  # noqa: E402
+from paper_2309_04671_b200 import GridBuffer  # noqa: E402
 
 
 def main():

@@ -213,6 +213,11 @@ def run_ours(args) -> None:
     from paper_2309_04671_b200 import plan_gpu
 
     ws, rank, local = dist_env()
+    if not os.environ.get("STKB_BENCH_ONE_DEVICE") and torch.cuda.device_count() < ws:
+        if rank == 0:  # one process per GPU: never time fewer GPUs than the line claims
+            print(json.dumps({"metric": METRIC, "value": None, "n_gpus": ws,
+                              "error": f"{ws} ranks but {torch.cuda.device_count()} visible GPUs"}), flush=True)
+        sys.exit(2)
     torch.cuda.set_device(local)
     if ws > 1 and args.watchdog > 0:
         # a rank that never returns (e.g. a neighbour died and its step flag never comes)
@@ -290,16 +295,22 @@ def run_ours(args) -> None:
             e = slab_e2e(builder, shape, dtype, K, sb.plan, sb.dist, local)
             slab_e2e = {"value": npts * K / e["seconds"] / 1e9, "unit": "GPts/s",
                         "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
+                        "h2d_bytes_per_call": e["h2d_bytes_per_call"], "d2h_bytes_per_call": e["d2h_bytes_per_call"],
                         "steps_per_call": K, "seconds": e["seconds"],
-                        "what": "slabs.run_slab per rank: H2D of the rank's slabs from pinned host memory, "
+                        "setup_in_timed_call": e["setup_in_timed_call"],
+                        "what": "slabs.run_slab per rank (slab engine allocated, IPC-connected and probed by a "
+                                "warm-up call, reused here): H2D of the rank's slabs from pinned host memory, "
                                 f"{K} steps with the {comm['transport']} halo exchange, D2H; wall clock, "
-                                "max over ranks"}
+                                "max over ranks; bytes per step = bytes per call / steps"}
+    per_rank = None
     if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        every = [None] * ws
+        dist.all_gather_object(every, (rank, float(ms), int(local_pts)))
+        per_rank = [{"rank": r, "ms": round(m, 4), "gpts_per_s": round(p * K / (m / 1e3) / 1e9, 3)}
+                    for r, m, p in sorted(every)]
+        ms = max(m for _, m, _ in every)  # the job's time: the slowest rank
     sec = ms / 1e3
     value = npts * K / sec / 1e9  # whole job: all ranks' points / max-over-ranks time
     per_step_ms = ms / K
@@ -326,12 +337,15 @@ def run_ours(args) -> None:
         e_sec = time.perf_counter() - t0
         from paper_2309_04671_b200.backend import LAST_RUN
 
-        e2e = {"value": npts * K / e_sec / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": LAST_RUN["h2d_bytes"],
-               "d2h_bytes_per_step": LAST_RUN["d2h_bytes"], "gpu_launches": LAST_RUN["launches"],
-               "steps_per_call": K, "seconds": e_sec,
+        e2e = {"value": npts * K / e_sec / 1e9, "unit": "GPts/s",
+               "h2d_bytes_per_step": LAST_RUN["h2d_bytes"] / K, "d2h_bytes_per_step": LAST_RUN["d2h_bytes"] / K,
+               "h2d_bytes_per_call": LAST_RUN["h2d_bytes"], "d2h_bytes_per_call": LAST_RUN["d2h_bytes"],
+               "gpu_launches": LAST_RUN["launches"], "steps_per_call": K, "seconds": e_sec,
+               "reused_domain": LAST_RUN.get("reused_domain"),
                "what": "one run_gpu(bound, plan, grids) call: H2D of the live input grids from pinned host "
                        f"memory (a zero-halo grid fully overwritten before any read needs no copy), {K} time "
-                       "steps (CUDA graph), D2H of every grid; wall clock"}
+                       "steps (CUDA graph), D2H of every grid; wall clock; bytes per step = bytes per call / "
+                       "steps (a time-stepping call moves its grids once)"}
         del grids, out
 
     # ------------------------------------------------------------ CPU baseline
@@ -386,10 +400,16 @@ def run_ours(args) -> None:
         }
         if comm:
             line["config"]["halo_exchange"] = comm
+        if per_rank is not None:
+            line["world_size"] = ws
+            line["per_rank"] = per_rank
         print(json.dumps(line), flush=True)
     if ws > 1 or args.force_slabs:
         import torch.distributed as dist
 
+        from paper_2309_04671_b200.slabs import release_slab_engines
+
+        release_slab_engines()
         dist.barrier()
         dist.destroy_process_group()
 
@@ -426,6 +446,28 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def launch_world(args, argv) -> int:
+    """``--gpus N`` outside torchrun: run this same command as N ranks, one process per
+    GPU (torch.distributed.run on 127.0.0.1), and return its exit code.  Under torchrun
+    the world size must equal --gpus."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+    return subprocess.run(cmd).returncode
+
+
+def world_error(args):
+    """None, or why this process's world does not match --gpus."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None and int(ws) != args.gpus:
+        return f"--gpus {args.gpus} but WORLD_SIZE={ws}"
+    return None
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -449,6 +491,12 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_world(args, sys.argv[1:]))
+    err = world_error(args)
+    if err and args.impl == "ours":
+        print(json.dumps({"metric": METRIC, "value": None, "n_gpus": args.gpus, "error": err}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -76,8 +76,20 @@ def run(dev_a: int, dev_b: int, steps: int = 3) -> dict:
     return {"ok": same, "devices": [dev_a, dev_b], "why": "" if same else "slab result differs from unsplit"}
 
 
+_VERDICTS: dict = {}  # (dev_a, dev_b) -> (ok, why): one child process per device pair and process
+PROBES_RUN = [0]
+
+
 def probe(dev_a: int, dev_b: int, timeout: float = 240.0) -> tuple:
-    """(ok, why) from a child process; never raises."""
+    """(ok, why) from a child process, cached per device pair; never raises."""
+    key = (int(dev_a), int(dev_b))
+    if key not in _VERDICTS:
+        PROBES_RUN[0] += 1
+        _VERDICTS[key] = _probe(dev_a, dev_b, timeout)
+    return _VERDICTS[key]
+
+
+def _probe(dev_a: int, dev_b: int, timeout: float) -> tuple:
     try:
         r = subprocess.run([sys.executable, "-m", "paper_2309_04671_b200.peer_probe", str(dev_a), str(dev_b)],
                            cwd=str(ROOT), capture_output=True, text=True, timeout=timeout)

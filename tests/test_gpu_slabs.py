@@ -203,10 +203,12 @@ def test_two_process_ipc_exchange_matches_unsplit_oracle(tmp_path, builder, shap
         assert rep.max_relative <= 1e-5, (n, rep.render())
 
 
-@pytest.mark.parametrize("scaling", ["strong", "weak"])
-def test_bench_multi_rank_path_runs(scaling):
-    """bench.py's N>1 path (SlabBench + run_slab e2e, fused exchange over CUDA IPC) under
-    torchrun with two ranks sharing cuda:0 and gloo collectives: code-path check, not timing."""
+@pytest.mark.parametrize("scaling,launcher", [("strong", "torchrun"), ("weak", "torchrun"), ("strong", "self")])
+def test_bench_multi_rank_path_runs(scaling, launcher):
+    """bench.py's N>1 path (SlabBench + run_slab e2e, fused exchange over CUDA IPC) with two
+    ranks sharing cuda:0 and gloo collectives, under torchrun or launched by bench.py itself
+    (``--gpus 2`` without torchrun): code-path check, not timing.  The e2e timed call adds
+    no engine, no IPC exchange and no peer probe."""
     import json
     import os
     import socket
@@ -220,6 +222,8 @@ def test_bench_multi_rank_path_runs(scaling):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--gpus", "2",
            "--steps", "4", "--warmup", "3", "--no-cpu", "--shape", "64,96,160", "--scaling", scaling]
+    if launcher == "self":
+        cmd = [sys.executable, os.path.join(root, "bench.py")] + cmd[cmd.index("--gpus"):]
     env = dict(os.environ, STKB_BENCH_ONE_DEVICE="1")
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
@@ -230,6 +234,8 @@ def test_bench_multi_rank_path_runs(scaling):
     assert d["scaling"] == scaling
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["config"]["halo_exchange"]["transport"] == "p2p"
+    assert d["world_size"] == 2 and [r["rank"] for r in d["per_rank"]] == [0, 1]
+    assert d["e2e"]["setup_in_timed_call"] == {"engines_created": 0, "ipc_connects": 0, "probes": 0}
 
 
 @pytest.mark.parametrize("world,builder,shape,steps", [

@@ -198,6 +198,14 @@ int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (le
  * sweeps need not stage them): stkb_launches counts it.  enable = 0 turns it off. */
 int stkb_set_fused_steps(stkb_domain *dom, int32_t enable);
 
+/* Several time steps per launch for small grids (on by default): when the step program
+ * is the Jacobi ping-pong `v = S(u); swap(u, v)` of a fast 3-D STAR map and the grid has
+ * at most max_points interior points (0 keeps the current limit, 2^25 by default),
+ * stkb_run launches up to 64 steps at a time; a grid barrier inside the kernel separates
+ * the steps (a cooperative launch: all CTAs resident).  Every grid ends bit-identical to
+ * single steps.  enable = 0 turns it off. */
+int stkb_set_multi_steps(stkb_domain *dom, int32_t enable, int64_t max_points);
+
 /* Let `device` read and write `peer`'s memory (cudaDeviceEnablePeerAccess; already
  * enabled is fine).  Used to wire in-process slab domains on different GPUs
  * (slabs.connect_local, the peer-pull probe); IPC-opened memory does not need it. */

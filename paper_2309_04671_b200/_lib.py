@@ -36,7 +36,7 @@ EXPORTS = (
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
     "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
     "stkb_flags_ipc_handle", "stkb_buffer_ptr", "stkb_flags_ptr", "stkb_ipc_open", "stkb_ipc_close", "stkb_set_peer",
-    "stkb_peer_signal", "stkb_peer_wait", "stkb_set_fused_steps", "stkb_enable_peer", "stkb_prepare",
+    "stkb_peer_signal", "stkb_peer_wait", "stkb_set_fused_steps", "stkb_set_multi_steps", "stkb_enable_peer", "stkb_prepare",
 )
 
 
@@ -137,6 +137,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_stream_wait_signal": [V, V, i32, i32],
         "stkb_set_max_ctas": [V, i32],
         "stkb_set_fused_steps": [V, i32],
+        "stkb_set_multi_steps": [V, i32, i64],
         "stkb_enable_peer": [i32, i32],
         "stkb_prepare": [V],
         "stkb_launch_map_pull": [V, i32],

@@ -272,6 +272,11 @@ class DeviceTarget:
         bit-identical to single steps, include/stkb200.h stkb_set_fused_steps)."""
         L.call("stkb_set_fused_steps", self.h, int(bool(enable)))
 
+    def set_multi_steps(self, enable: bool, max_points: int = 0) -> None:
+        """Several ping-pong steps per launch on small grids (default on; bit-identical
+        to single steps, include/stkb200.h stkb_set_multi_steps)."""
+        L.call("stkb_set_multi_steps", self.h, int(bool(enable)), ctypes.c_int64(int(max_points)))
+
     def run(self, steps: int) -> None:
         L.call("stkb_run", self.h, ctypes.c_int64(int(steps)))
         self.total_launches = getattr(self, "total_launches", 0) + self.launches()

@@ -79,6 +79,13 @@ struct StarArgs {
     // when bit 1 is — over NVLink, in place of this slab's own halo planes
     int32_t pull;
     int32_t pull_lo_n0;
+    // several time steps in one launch (small grids, Jacobi ping-pong): step s reads
+    // src (even s) / dst (odd s) and writes the other; a grid barrier (step_arrive)
+    // separates the steps; work_counter then holds one counter per step
+    int32_t n_steps;
+    T* dst_alt;                  // odd steps write here (the even steps' src buffer)
+    const int32_t* halo_nz_alt;  // halo flag of dst (the src of odd steps)
+    int32_t* step_arrive;        // CTAs that stored all their items of a step (cumulative)
     T cb[729];                 // BOX: dense (2R+1)^3 coefficients, [dz][dy][dx], R <= 4 (last: the
                                // other fields keep their parameter-bank offsets)
 };
@@ -133,6 +140,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
           "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+
+// make this thread's generic-proxy global writes visible to later async-proxy (TMA)
+// reads, and order an acquire before this thread's own TMA reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -216,6 +235,8 @@ struct StarLaunch {
     int* signal_items;     // out: number of signal items of this launch
     const int32_t* frozen_nz;  // fused sweeps: != 0 when v's frozen values next to the box are not all zero
     int band_pct = 0;      // item order: tile-row bands of band_pct % of a wave (0 = z-major)
+    int n_steps = 1;       // > 1: a multi-step launch (StarArgs::n_steps); counters = n_steps work
+    int32_t* step_counters = nullptr;  // counters followed by the step-arrive counter (zeroed here)
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);

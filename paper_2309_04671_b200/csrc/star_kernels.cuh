@@ -210,14 +210,18 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
             // a src whose halo is all zero is read through the interior-only map: the TMA
             // zero-fills the halo instead of fetching it (the padded grid's own halo is ~1.5 %
             // of a 1024^3 step's reads)
-            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
-            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
-                      iz = interior ? int(a.g.order0) : 0;
-            const CUtensorMap* own = interior ? &tm_int : &tm_src;
-            prefetch_tmap(own);
+            const int nsteps = PULL ? 1 : a.n_steps;
+            const bool interior0 = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            // multi-step launches (never PULL): odd steps read the dst buffer through tm_lo (full)
+            // or tm_hi (interior only)
+            const bool interior1 = nsteps > 1 && a.halo_nz_alt &&
+                                   *reinterpret_cast<const volatile int32_t*>(a.halo_nz_alt) == 0;
+            prefetch_tmap(interior0 ? &tm_int : &tm_src);
             if constexpr (PULL) {
                 if (a.pull & 1) prefetch_tmap(&tm_lo);
                 if (a.pull & 2) prefetch_tmap(&tm_hi);
+            } else if (nsteps > 1) {
+                prefetch_tmap(interior1 ? &tm_hi : &tm_lo);
             }
             if constexpr (FORM == FORM_WAVE) {
                 prefetch_tmap(&tm_ctr);
@@ -225,67 +229,83 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 prefetch_tmap(&tm_vel);
             }
             uint32_t it = 0;
-            // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
-            // order, so CTAs working at the same time stream neighbouring tiles and
-            // share their halo rows through L2
-            while (true) {
-                const int item = atomicAdd(a.work_counter, 1);
-                if (item >= a.n_items) {
-                    const uint32_t s = it % STAGES;
-                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
-                    stage_item[s] = -1;  // sentinel: no more work
-                    mbar_arrive(&full[s]);
-                    break;
+            for (int step = 0; step < nsteps; ++step) {
+                const bool odd = (step & 1) != 0;
+                const bool interior = odd ? interior1 : interior0;
+                const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                          iz = interior ? int(a.g.order0) : 0;
+                const CUtensorMap* own = odd ? (interior ? &tm_hi : &tm_lo) : (interior ? &tm_int : &tm_src);
+                if (step > 0) {
+                    // grid barrier: every CTA has stored its items of the previous step (they
+                    // published them with a release after a proxy fence); then order this
+                    // thread's TMA reads after the acquire
+                    const int32_t target = int32_t(gridDim.x) * step;
+                    while (ld_acquire_gpu(a.step_arrive) < target) __nanosleep(64);
+                    fence_proxy_async_global();
                 }
-                int tx, ty, tz;
-                decode_item(a, item, tx, ty, tz);
-                const int x0 = a.x0base + tx * BX;
-                const int y0 = a.box.lo1 + ty * BY;
-                const int z0 = a.zs[2 * tz];
-                const int z1 = a.zs[2 * tz + 1];
-                const int c0 = int(a.g.lead) + x0 - RA;
-                const int c1 = y0 + int(a.g.order) - R;
-                for (int q = z0 - R; q < z1 + R; ++q, ++it) {
-                    const uint32_t s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1u;
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    stage_item[s] = item;
-                    T* st = tiles + size_t(s) * C::STAGE_ELEMS;
-                    // src plane q: this slab's own (incl. its halo), or a neighbour's over NVLink
-                    const CUtensorMap* hm = own;
-                    int hz = q + int(a.g.order0) - iz;
-                    int hx = c0 - ix, hy = c1 - iy;
-                    if constexpr (PULL) {
-                        if (q < 0 && (a.pull & 1)) {
-                            hm = &tm_lo;
-                            hz = q + a.pull_lo_n0 + int(a.g.order0);
-                            hx = c0;
-                            hy = c1;
-                        } else if (q >= int(a.g.n0) && (a.pull & 2)) {
-                            hm = &tm_hi;
-                            hz = q - int(a.g.n0) + int(a.g.order0);
-                            hx = c0;
-                            hy = c1;
+                // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
+                // order, so CTAs working at the same time stream neighbouring tiles and
+                // share their halo rows through L2
+                while (true) {
+                    const int item = atomicAdd(a.work_counter + step, 1);
+                    if (item >= a.n_items) break;
+                    int tx, ty, tz;
+                    decode_item(a, item, tx, ty, tz);
+                    const int x0 = a.x0base + tx * BX;
+                    const int y0 = a.box.lo1 + ty * BY;
+                    const int z0 = a.zs[2 * tz];
+                    const int z1 = a.zs[2 * tz + 1];
+                    const int c0 = int(a.g.lead) + x0 - RA;
+                    const int c1 = y0 + int(a.g.order) - R;
+                    const int tag = item + step * a.n_items;  // the consumers recover the step
+                    for (int q = z0 - R; q < z1 + R; ++q, ++it) {
+                        const uint32_t s = it % STAGES;
+                        const uint32_t ph = (it / STAGES) & 1u;
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        stage_item[s] = tag;
+                        T* st = tiles + size_t(s) * C::STAGE_ELEMS;
+                        // src plane q: this slab's own (incl. its halo), or a neighbour's over NVLink
+                        const CUtensorMap* hm = own;
+                        int hz = q + int(a.g.order0) - iz;
+                        int hx = c0 - ix, hy = c1 - iy;
+                        if constexpr (PULL) {
+                            if (q < 0 && (a.pull & 1)) {
+                                hm = &tm_lo;
+                                hz = q + a.pull_lo_n0 + int(a.g.order0);
+                                hx = c0;
+                                hy = c1;
+                            } else if (q >= int(a.g.n0) && (a.pull & 2)) {
+                                hm = &tm_hi;
+                                hz = q - int(a.g.n0) + int(a.g.order0);
+                                hx = c0;
+                                hy = c1;
+                            }
+                        }
+                        if constexpr (FORM == FORM_WAVE) {
+                            const int z = q - R;  // output plane completed at this step
+                            const bool out = (z >= z0);
+                            mbar_arrive_expect_tx(&full[s], C::HALO_BYTES + (out ? 3 * C::CTR_BYTES : 0));
+                            tma_load_3d(st, hm, &full[s], hx, hy, hz);
+                            if (out) {
+                                const int cx = int(a.g.lead) + x0;
+                                const int cy = y0 + int(a.g.order);
+                                const int cz = z + int(a.g.order0);
+                                tma_load_3d(st + C::HALO_ELEMS, &tm_ctr, &full[s], cx, cy, cz);
+                                tma_load_3d(st + C::HALO_ELEMS + C::CTR_ELEMS, &tm_prev, &full[s], cx, cy, cz);
+                                tma_load_3d(st + C::HALO_ELEMS + 2 * C::CTR_ELEMS, &tm_vel, &full[s], cx, cy, cz);
+                            }
+                        } else {
+                            mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
+                            tma_load_3d(st, hm, &full[s], hx, hy, hz);
                         }
                     }
-                    if constexpr (FORM == FORM_WAVE) {
-                        const int z = q - R;  // output plane completed at this step
-                        const bool out = (z >= z0);
-                        mbar_arrive_expect_tx(&full[s], C::HALO_BYTES + (out ? 3 * C::CTR_BYTES : 0));
-                        tma_load_3d(st, hm, &full[s], hx, hy, hz);
-                        if (out) {
-                            const int cx = int(a.g.lead) + x0;
-                            const int cy = y0 + int(a.g.order);
-                            const int cz = z + int(a.g.order0);
-                            tma_load_3d(st + C::HALO_ELEMS, &tm_ctr, &full[s], cx, cy, cz);
-                            tma_load_3d(st + C::HALO_ELEMS + C::CTR_ELEMS, &tm_prev, &full[s], cx, cy, cz);
-                            tma_load_3d(st + C::HALO_ELEMS + 2 * C::CTR_ELEMS, &tm_vel, &full[s], cx, cy, cz);
-                        }
-                    } else {
-                        mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
-                        tma_load_3d(st, hm, &full[s], hx, hy, hz);
-                    }
                 }
+                // end of a step (-2) or of the launch (-1): a stage without data
+                const uint32_t s = it % STAGES;
+                mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                stage_item[s] = step + 1 < nsteps ? -2 : -1;
+                mbar_arrive(&full[s]);
+                ++it;
             }
         }
         return;
@@ -310,10 +330,25 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
     const int64_t pitch = a.g.pitch, plane = a.g.plane;
 
     while (true) {
-        // the producer tags every stage with its work item; -1 ends the kernel
+        // the producer tags every stage with its work item; -1 ends the kernel, -2 a step
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
-        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);  // warp-uniform: uniform branches
-        if (item < 0) break;
+        const int tag = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);  // warp-uniform: uniform branches
+        if (tag == -1) break;
+        if (tag == -2) {
+            // multi-step launch: this CTA's outputs of the step are stored; publish them
+            // (visible to other CTAs' TMA reads) and count the CTA in the grid barrier
+            __threadfence();
+            fence_proxy_async_global();
+            asm volatile("bar.sync 1, %0;" ::"r"(NWY * 32) : "memory");
+            if (threadIdx.x == 0) atomicAdd(a.step_arrive, 1);
+            __syncwarp();
+            mbar_arrive_lane0(&empty[it % STAGES], lane);
+            ++it;
+            continue;
+        }
+        const int step = a.n_steps > 1 ? tag / a.n_items : 0;
+        const int item = tag - step * a.n_items;
+        T* const dst_step = (step & 1) ? a.dst_alt : a.dst;
         int tx, ty, tz;
         decode_item(a, item, tx, ty, tz);
         const int x0 = a.x0base + tx * BX;
@@ -326,7 +361,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         const bool x_full = (x >= a.box.lo2) && (x + VEC <= a.box.hi2);
         const bool x_any = (x + VEC > a.box.lo2) && (x < a.box.hi2);
         // output address of row jr0 at plane z: dst0 + (z + order0) * plane + j * pitch
-        T* const dst0 = a.dst + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x;
+        T* const dst0 = dst_step + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x;
 
         // the plane loop is unrolled by 2R+1 so the accumulator ring slots are static
         // registers; the wide dense boxes (R > 2: 343 / 729 taps per plane) keep one plane
@@ -678,6 +713,27 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     a.n_items = tiles * a.n_tz;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;
+    if (L.n_steps > 1 && !PULL) {
+        // several steps, one grid barrier between them: every CTA must be resident at once,
+        // which the cooperative launch guarantees (it fails instead of deadlocking)
+        a.n_steps = L.n_steps;
+        a.work_counter = L.step_counters;
+        a.step_arrive = L.step_counters + L.n_steps;
+        cudaError_t e = cudaMemsetAsync(L.step_counters, 0, (L.n_steps + 1) * sizeof(int32_t), stream);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], a);
+    }
+    a.n_steps = 1;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
     kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], a);

@@ -74,6 +74,7 @@ int fail(int code, const std::string& msg) {
 
 constexpr int kMaxTags = 64;
 constexpr int kMaxMaps = 256;
+constexpr int kMaxMultiSteps = 64;  // time steps per multi-step launch
 constexpr int kFrozenFlag = kMaxTags + 2 * kMaxMaps;  // d_flags slot: v's frozen ring is not all zero
 constexpr int kHaloFlag = kFrozenFlag + 4;            // per buffer: its halo may hold non-zero values
 constexpr int kNumFlags = kHaloFlag + 40;
@@ -164,6 +165,10 @@ struct stkb_domain {
     // halo flags (d_flags[kHaloFlag + buffer]): 0 = that buffer's halo is all +0, so its stencil
     // reads go through an interior-only tensor map; recomputed when ext_writes moved
     int64_t halo_epoch = 0;
+    // several ping-pong steps per launch for small grids (star_kernels.cuh, StarArgs::n_steps)
+    int32_t* d_multi = nullptr;    // per-step work counters + the step-arrive counter
+    int64_t multi_max_points = int64_t(1) << 25;  // STKB_MULTI_POINTS: grids up to this many points
+    bool multi = true;             // STKB_MULTI=0 disables
     bool halo_external = false;  // z-slab machinery writes halo planes (exchange, peers): full maps only
     std::map<std::tuple<int, int, int>, CUtensorMap> tmaps_int;  // (buffer, box w, box h), interior only
 };
@@ -354,7 +359,7 @@ struct RangeSpec {
 
 template <typename T>
 int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind,
-                    const RangeSpec& rs = RangeSpec(), bool pull = false) {
+                    const RangeSpec& rs = RangeSpec(), bool pull = false, int n_steps = 1) {
     const stkb_map_desc& d = op.d;
     if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
     if (int rc = ensure_halo_flags(dom)) return rc;
@@ -414,6 +419,17 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         }
         a.pull_lo_n0 = int32_t(dom->peer[0].n0);
     }
+    if (n_steps > 1) {
+        // multi-step ping-pong: odd steps read the dst buffer (maps 4 / 5) and write src's
+        const int db = bind[d.dst];
+        const CUtensorMap *m_alt = nullptr, *m_alt_int = nullptr;
+        if ((rc = encode_map(dom, db, lw, lh, &m_alt))) return rc;
+        if ((rc = encode_map_int(dom, db, lw, lh, &m_alt_int))) return rc;
+        maps[4] = *m_alt;
+        maps[5] = *m_alt_int;
+        a.dst_alt = static_cast<T*>(dom->bufs[sb]);
+        a.halo_nz_alt = dom->halo_external ? nullptr : dom->d_flags + kHaloFlag + db;
+    }
     if (d.kind == STKB_MAP_WAVE) {
         const CUtensorMap *mc, *mp, *mv;
         if ((rc = encode_map(dom, sb, bx, by, &mc))) return rc;
@@ -441,6 +457,12 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.n_signal_ranges = rs.n_signal;
     L.signal = dom->d_flags + kMaxTags + kMaxMaps + op.slot;
     L.signal_items = rs.signal_items;
+    if (n_steps > 1) {
+        if (!dom->d_multi && cudaMalloc(&dom->d_multi, (kMaxMultiSteps + 1) * sizeof(int32_t)) != cudaSuccess)
+            return fail(STKB_ERR_CUDA, "multi-step counters");
+        L.n_steps = n_steps;
+        L.step_counters = dom->d_multi;
+    }
     cudaError_t e;
     if constexpr (sizeof(T) == 4) e = launch_star_f32(L, a, dom->stream);
     else e = launch_star_f64(L, a, dom->stream);
@@ -526,6 +548,25 @@ const MapOp* tb_map(const stkb_domain* dom) {
     // radius 1 only: at radius 2 the v rows each warp recomputes (TY2 + 4 for TY2 outputs
     // within the register budget) cost more than the halved HBM traffic saves (measured)
     if (d.kind != STKB_MAP_STAR || d.radius != 1 || d.precision != STKB_PREC_FAST) return nullptr;
+    if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;
+    if (d.lo[0] >= d.hi[0] || d.lo[1] >= d.hi[1] || d.lo[2] >= d.hi[2]) return nullptr;
+    return &op;
+}
+
+// The step program is `v = S(u); swap(u, v)` with S a fast 3-D STAR map on a small grid
+// (at most multi_max_points interior points: a step is a few microseconds, so launch
+// and pipeline start-up dominate): several steps run per launch, separated by a grid
+// barrier inside the kernel (StarArgs::n_steps).  Per point the arithmetic is the
+// single-step kernel's, so every grid ends bit-identical to single steps.
+const MapOp* multi_map(const stkb_domain* dom) {
+    if (!dom->multi || dom->desc.ndim != 3 || dom->prog.size() != 2 || dom->halo_external) return nullptr;
+    if (dom->g.n0 * dom->g.n1 * dom->g.n2 > dom->multi_max_points) return nullptr;
+    const ProgOp& m = dom->prog[0];
+    const ProgOp& w = dom->prog[1];
+    if (m.kind != 0 || w.kind != 1) return nullptr;
+    const MapOp& op = dom->maps[m.map];
+    const stkb_map_desc& d = op.d;
+    if (d.kind != STKB_MAP_STAR || d.precision != STKB_PREC_FAST) return nullptr;
     if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;
     if (d.lo[0] >= d.hi[0] || d.lo[1] >= d.hi[1] || d.lo[2] >= d.hi[2]) return nullptr;
     return &op;
@@ -669,6 +710,8 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_BAND")) dom->band_pct = atoi(s);
     if (const char* s = getenv("STKB_PRESCALE")) dom->prescale = atoi(s) != 0;
     if (const char* s = getenv("STKB_TB")) dom->tb = atoi(s) != 0;
+    if (const char* s = getenv("STKB_MULTI")) dom->multi = atoi(s) != 0;
+    if (const char* s = getenv("STKB_MULTI_POINTS")) dom->multi_max_points = atoll(s);
     *out = dom;
     return STKB_OK;
 }
@@ -688,6 +731,7 @@ int stkb_domain_destroy(stkb_domain* dom) {
     if (dom->d_partials) cudaFree(dom->d_partials);
     if (dom->d_stage) cudaFree(dom->d_stage);
     if (dom->d_peer_flags) cudaFree(dom->d_peer_flags);
+    if (dom->d_multi) cudaFree(dom->d_multi);
     if (dom->ev0) cudaEventDestroy(dom->ev0);
     if (dom->ev1) cudaEventDestroy(dom->ev1);
     if (dom->own_stream) cudaStreamDestroy(dom->own_stream);
@@ -1076,6 +1120,23 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
     const int period = binding_period(dom);
     const bool graphs_ok = period > 0 && getenv("STKB_NO_GRAPH") == nullptr;
     if (int rc = ensure_halo_flags(dom)) return rc;  // before the timed events
+    if (const MapOp* mm = steps >= 2 ? multi_map(dom) : nullptr) {
+        CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
+        while (done < steps) {
+            const int n = int(std::min<int64_t>(kMaxMultiSteps, steps - done));
+            const int rc = dom->desc.dtype == STKB_F32
+                               ? launch_star_map<float>(dom, *mm, dom->binding, RangeSpec(), false, n)
+                               : launch_star_map<double>(dom, *mm, dom->binding, RangeSpec(), false, n);
+            if (rc) return rc;
+            ++launches;
+            if (n & 1) std::swap(dom->binding[mm->d.src], dom->binding[mm->d.dst]);
+            done += n;
+        }
+        CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
+        dom->timed = true;
+        dom->last_launches = launches;
+        return STKB_OK;
+    }
     if (const MapOp* tb = steps >= 4 ? tb_map(dom) : nullptr) {
         // fused sweeps for all but the last 2..3 steps, which run as single steps so
         // that v ends up holding its own final value
@@ -1510,6 +1571,14 @@ int stkb_enable_peer(int32_t device, int32_t peer) {
 int stkb_set_fused_steps(stkb_domain* dom, int32_t enable) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     dom->tb = enable != 0;
+    return STKB_OK;
+}
+
+int stkb_set_multi_steps(stkb_domain* dom, int32_t enable, int64_t max_points) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (max_points < 0) return fail(STKB_ERR_ARG, "max_points must be >= 0");
+    dom->multi = enable != 0;
+    if (max_points > 0) dom->multi_max_points = max_points;
     return STKB_OK;
 }
 

@@ -40,6 +40,7 @@ def _device_run(bound, grids, steps, fused, box=None):
         for n in ("u", "v"):
             dt.upload(n, grids[n].data)
         dt.set_fused_steps(fused)
+        dt.set_multi_steps(False)  # small grids would take the multi-step launch instead
         if box is None:
             dt.set_program(body)
         else:  # one map over a sub-box of the interior, then the swap
@@ -110,7 +111,11 @@ def test_fused_sweeps_zero_and_nonzero_halo_bitwise(halo):
 
 @pytest.mark.parametrize("builder,dtype,shape", [("jacobi7", "f32", (96, 80, 200)), ("star3d1r", "f64", (33, 40, 70)),
                                                  ("star3d1r_norm", "f32", (40, 50, 300))])
-def test_fused_run_gpu_within_tolerance_vs_c_oracle(builder, dtype, shape):
+def test_fused_run_gpu_within_tolerance_vs_c_oracle(builder, dtype, shape, monkeypatch):
+    from paper_2309_04671_b200 import release_device_cache
+
+    monkeypatch.setenv("STKB_MULTI", "0")  # these grids are small enough for multi-step launches
+    release_device_cache()
     steps = 12
     bound, decls = corpus.config_target(builder, shape, steps, dtype)
     grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
@@ -150,6 +155,7 @@ def test_fused_repeated_runs_and_scratch_reuse():
             for n in ("u", "v"):
                 dt.upload(n, grids[n].data)
             dt.set_fused_steps(fused)
+            dt.set_multi_steps(False)  # small grids would take the multi-step launch instead
             dt.set_program(body)
             dt.run(6)
             dt.run(8)
@@ -201,6 +207,7 @@ def test_fused_pair_invalidated_by_writes_outside_the_box(steps):
             for n in ("u", "v"):
                 dt.upload(n, grids[n].data)
             dt.set_fused_steps(fused)
+            dt.set_multi_steps(False)  # small grids would take the multi-step launch instead
             for _ in range(3):
                 d = dt.compile_map(bmap, 0, box=box)
                 L.call("stkb_program_reset", dt.h)

@@ -240,7 +240,8 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     // published them with a release after a proxy fence); then order this
                     // thread's TMA reads after the acquire
                     const int32_t target = int32_t(gridDim.x) * step;
-                    while (ld_acquire_gpu(a.step_arrive) < target) __nanosleep(64);
+                    while (ld_acquire_gpu(a.step_arrive) < target) {
+                    }
                     fence_proxy_async_global();
                 }
                 // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
@@ -686,6 +687,11 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     for (int i = nsig; i < nr; ++i) main_n0 = std::max(main_n0, rhi[i] - rlo[i]);
     if (L.lz > 0) {
         a.lz = L.lz;
+    } else if (L.n_steps > 1 && main_n0 > 0 && tiles < ctas) {
+        // multi-step launch on a small grid: one item per CTA and step, the shortest chunks
+        // that still fit in one wave (every step waits for its slowest CTA)
+        const int per_tile = std::max(1, ctas / tiles);
+        a.lz = (main_n0 + per_tile - 1) / per_tile;
     } else if (main_n0 > 0) {
         int ntz;
         a.lz = choose_lz(main_n0, tiles, ctas, R, &ntz);
@@ -699,7 +705,7 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
         a.zs[2 * k + 1] = rhi[i];
     }
     for (int i = nsig; i < nr && k < kMaxChunks; ++i)
-        k = chunk_range(rlo[i], rhi[i] - rlo[i], a.lz, tiles, ctas, L.taper, a.zs, k);
+        k = chunk_range(rlo[i], rhi[i] - rlo[i], a.lz, tiles, ctas, L.taper && L.n_steps <= 1, a.zs, k);
     a.n_tz = k;
     a.n_signal = nsig;
     // bands of ~one wave (STKB_BAND = wave fraction in %, 0 = plain z-major order)

@@ -207,44 +207,7 @@ class DeviceTarget:
         return self.map_desc(plan, tag, box)
 
     def map_desc(self, plan: MapPlan, tag: int, box: Optional[tuple] = None) -> L.MapDesc:
-        d = L.MapDesc()
-        d.tag = tag
-        d.precision = L.STKB_PREC_FAST
-        d.src = d.dst = d.prev = d.vel = -1
-        bx = box if box is not None else plan.box
-        for i, (lo, hi) in enumerate(bx):
-            d.lo[i], d.hi[i] = lo, hi
-        if plan.kind in ("star", "wave", "box"):
-            d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX}[plan.kind]
-            d.radius = plan.radius
-            d.src, d.dst = self.index[plan.src], self.index[plan.dst]
-            if plan.kind == "wave":
-                d.prev, d.vel = self.index[plan.prev], self.index[plan.vel]
-                d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
-            if plan.kind == "box" and len(plan.coef) > 125:  # 3-D box of radius 3..4
-                ext = np.ascontiguousarray(np.array(plan.coef, dtype=np.float64))
-                d._keep_ext = ext  # alive until stkb_program_add_map has copied it
-                d.box_coef_ext = ext.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-            else:
-                for i, c in enumerate(plan.coef):
-                    if plan.kind == "box":
-                        d.box_coef[i] = c
-                    else:
-                        d.coef[i] = c
-            d.divisor = plan.divisor
-        else:
-            d.kind = L.STKB_MAP_EXPR
-            d.n_args = len(plan.args)
-            for i, g in enumerate(plan.args):
-                d.args[i] = self.index[g]
-            flat = np.ascontiguousarray(np.array(plan.code, dtype=np.int32).reshape(-1))
-            consts = np.ascontiguousarray(np.array(plan.consts if plan.consts else [0.0], dtype=np.float64))
-            d.n_code = len(plan.code)
-            d.code = flat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-            d.n_consts = len(plan.consts)
-            d.consts = consts.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-            d._keep = (flat, consts)  # alive until stkb_program_add_map copied them
-        return d
+        return map_desc_for(plan, self.index, tag, box)
 
     def set_program(self, body: tuple) -> None:
         """Make ``body`` (maps and swaps) the step program, unless it already is."""
@@ -328,6 +291,49 @@ class DeviceTarget:
                         self.execute(body, bindings)
             else:
                 raise ExecutionError(f"unsupported statement {stmt!r}")
+
+
+def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = None) -> L.MapDesc:
+    """The C-ABI map descriptor (include/stkb200.h stkb_map_desc) of a matched map;
+    ``index`` maps grid names to domain names (0..n_grids-1)."""
+    d = L.MapDesc()
+    d.tag = tag
+    d.precision = L.STKB_PREC_FAST
+    d.src = d.dst = d.prev = d.vel = -1
+    bx = box if box is not None else plan.box
+    for i, (lo, hi) in enumerate(bx):
+        d.lo[i], d.hi[i] = lo, hi
+    if plan.kind in ("star", "wave", "box"):
+        d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX}[plan.kind]
+        d.radius = plan.radius
+        d.src, d.dst = index[plan.src], index[plan.dst]
+        if plan.kind == "wave":
+            d.prev, d.vel = index[plan.prev], index[plan.vel]
+            d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
+        if plan.kind == "box" and len(plan.coef) > 125:  # 3-D box of radius 3..4
+            ext = np.ascontiguousarray(np.array(plan.coef, dtype=np.float64))
+            d._keep_ext = ext  # alive until stkb_program_add_map has copied it
+            d.box_coef_ext = ext.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        else:
+            for i, c in enumerate(plan.coef):
+                if plan.kind == "box":
+                    d.box_coef[i] = c
+                else:
+                    d.coef[i] = c
+        d.divisor = plan.divisor
+    else:
+        d.kind = L.STKB_MAP_EXPR
+        d.n_args = len(plan.args)
+        for i, g in enumerate(plan.args):
+            d.args[i] = index[g]
+        flat = np.ascontiguousarray(np.array(plan.code, dtype=np.int32).reshape(-1))
+        consts = np.ascontiguousarray(np.array(plan.consts if plan.consts else [0.0], dtype=np.float64))
+        d.n_code = len(plan.code)
+        d.code = flat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        d.n_consts = len(plan.consts)
+        d.consts = consts.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        d._keep = (flat, consts)  # alive until stkb_program_add_map copied them
+    return d
 
 
 def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Optional[str] = None,

@@ -320,3 +320,44 @@ def test_one_d_maps(template):
         assert np.array_equal(got[n].data, ref[n].data), n
     with pytest.raises(sk_executor.ExecutionError, match="2D or 3D"):
         run_gpu(bound, sk_planning.plan_gpu(info, {"template": "unroll"}), grids)
+
+
+# -- criterion 10 (tests/test_acceptance.py:304-382): the compiled C-ABI artifact ----------
+def _run_compiled(artifact, entry, grids, iters, tmp):
+    """The reference harness (test_acceptance.py:322-343), restated: compile the
+    artifact's C with a plain `cc -O2 -fPIC -shared`, call `entry(T*..., int64 iter)`."""
+    import ctypes
+    import shutil
+
+    source = tmp / artifact.files[0][0]
+    source.write_text(artifact.files[0][1])
+    lib_path = tmp / (source.stem + ".so")
+    cc = shutil.which("cc") or shutil.which("gcc")
+    subprocess.run([cc, "-O2", "-fPIC", "-shared", str(source), "-o", str(lib_path)], check=True, capture_output=True)
+    lib = ctypes.CDLL(str(lib_path))
+    fn = getattr(lib, entry)
+    buffers = {name: np.ascontiguousarray(buf.padded.copy()) for name, buf in grids.items()}
+    args = [buffers[name].ctypes.data_as(ctypes.POINTER(ctypes.c_float)) for name in buffers]
+    fn.argtypes = [ctypes.POINTER(ctypes.c_float)] * len(buffers) + [ctypes.c_int64]
+    fn.restype = None
+    fn(*args, ctypes.c_int64(iters))
+    return buffers
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_criterion_10_harness_drives_the_library(tmp_path, precision):
+    """shim.emit gives the reference's own C entry `run_<target>(float*..., int64_t iter)`
+    over libstkb200.so: the criterion-10 harness compiles and calls it unchanged."""
+    from paper_2309_04671_b200 import shim
+
+    for name, shape in (("star2d4r", (32, 32)), ("star3d2r", (12, 12, 12)), ("j3d27pt", (10, 12, 14))):
+        iters = 3
+        unit = make_unit(name, shape=shape, iters=iters)
+        grids = make_grids(unit, seed=77)
+        reference = sk_executor.run_target(unit, grids)
+        artifact = shim.emit(unit, precision=precision)
+        assert artifact.entry == f"run_target_{name}"
+        out = _run_compiled(artifact, artifact.entry, grids, iters, tmp_path)
+        for n in reference:
+            got = sk_grids.GridBuffer("f32", shape, unit.grids[0].order, out[n])
+            check(reference[n], got, precision, exact_bitwise=True)

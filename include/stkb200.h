@@ -51,6 +51,10 @@ extern "C" {
 #define STKB_MAP_EXPR 3 /* any kernel: bytecode evaluated in float64, parse order,
                            one rounding per store (bit-identical to run_target,
                            executor.py:267-286) */
+#define STKB_MAP_XSTAR 5 /* exact star: dst = ((c0*src[0] + c_1*src[o_1]) + ... ) [/ divisor] in
+                            float64 with the terms in the corpus order (centre, then the star
+                            offsets sorted), one rounding per store: bit-identical to run_target
+                            at streaming speed; 3-D, radius 1..4, coef layout as STAR */
 
 /* step-program execution precision for STAR/WAVE maps */
 #define STKB_PREC_FAST 0 /* accumulate in the grid dtype with FMA (tolerance-checked) */

@@ -303,8 +303,9 @@ def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = No
     bx = box if box is not None else plan.box
     for i, (lo, hi) in enumerate(bx):
         d.lo[i], d.hi[i] = lo, hi
-    if plan.kind in ("star", "wave", "box"):
-        d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX}[plan.kind]
+    if plan.kind in ("star", "wave", "box", "xstar"):
+        d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX,
+                  "xstar": L.STKB_MAP_XSTAR}[plan.kind]
         d.radius = plan.radius
         d.src, d.dst = index[plan.src], index[plan.dst]
         if plan.kind == "wave":

@@ -90,6 +90,14 @@ struct StarArgs {
                                // other fields keep their parameter-bank offsets)
 };
 
+// coefficients of the exact star kernel (star_exact.cuh): the reference's float64 constants
+struct XstarCoef {
+    double c0;
+    double cm[3][4];  // [axis][m-1] coefficient of offset -m
+    double cp[3][4];  // [axis][m-1] coefficient of offset +m
+    double divisor;   // 0: none, else the sum is divided by it (IEEE division, as numpy does)
+};
+
 // ---------------------------------------------------------------------------
 // mbarrier / TMA PTX wrappers (sm_90+ ISA, used here for sm_100a)
 
@@ -241,4 +249,7 @@ struct StarLaunch {
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
 cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
+cudaError_t launch_exact_f32(const StarLaunch& L, const StarArgs<float>& a, const XstarCoef& xc, cudaStream_t s);
+cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, const XstarCoef& xc, cudaStream_t s);
+int exact_tile(int dtype, int radius, int* bx, int* by, int* halo_x);
 }  // namespace stkb

@@ -1,0 +1,283 @@
+// Exact 2.5D d0-streaming star kernel: the reference's own arithmetic at streaming speed.
+//
+// The reference oracle (run_target, executor.py:56-138, :222-286) evaluates a map in
+// float64, node by node in parse order, and rounds once to the grid dtype.  For the
+// canonical star kernels — the corpus form (corpus.py:77-120)
+//     v.at(0..).set(c0*u.at(0..) + c1*u.at(o1) + ... + cn*u.at(on))    [/ D]
+// with the offsets in sorted order after the centre (corpus.py:77-90) — that is
+//     acc = c0*u0;  acc = acc + c_k*u_k  (k = 1..n, each product and sum rounded in f64);
+//     acc = acc / D;  v = (T)acc.
+// This kernel performs exactly those IEEE operations (DMUL, DADD, DDIV with explicit
+// rounding, no contraction), in exactly that order, so its results are bit-identical to
+// run_target — not just within tolerance — while keeping the streaming structure of
+// star_kernels.cuh: TMA plane boxes into an mbarrier ring, persistent CTAs, the dynamic
+// work-item scheduler.
+//
+// Sorted star offsets put the d0 taps around the in-plane ones:
+//     centre, (-R..-1, 0, 0), (0, -R..-1, 0), (0, 0, -R..-1), (0, 0, 1..R), (0, 1..R, 0),
+//     (1..R, 0, 0)
+// so an output plane o can start only when its own plane arrives (the centre product comes
+// first): the d0-negative taps are taken from a ring of the previous R planes' centre
+// values (held in registers, converted to f64 once), the in-plane taps from the staged
+// tile, and the d0-positive taps are added one per arriving plane o+1..o+R to a ring of R
+// partial sums (f64).  One output row per warp keeps the f64 rings in registers.
+#pragma once
+
+#include "star_kernels.cuh"
+
+namespace stkb {
+
+template <typename T, int R>
+struct XstarCfg {
+    static constexpr int VEC = 16 / sizeof(T);
+    static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
+    static constexpr int NWY = 15;  // consumer warps, one output row each
+    static constexpr int BX = 32 * VEC;
+    static constexpr int BY = NWY;
+    static constexpr int SW = BX + 2 * RA;
+    static constexpr int SH = BY + 2 * R;
+    static constexpr int HALO_ELEMS = ((SW * SH * int(sizeof(T)) + 127) / 128) * 128 / int(sizeof(T));
+    static constexpr uint32_t HALO_BYTES = SW * SH * sizeof(T);
+    static constexpr uint32_t STAGE_BYTES = HALO_ELEMS * sizeof(T);
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+    static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
+                                   STAGES * sizeof(int32_t);
+    static constexpr int THREADS = (NWY + 1) * 32;
+};
+
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T, int R, bool DIV>
+__global__ void __launch_bounds__((XstarCfg<T, R>::NWY + 1) * 32, 1)
+star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
+                  const __grid_constant__ StarArgs<T> a, const __grid_constant__ XstarCoef xc) {
+    using C = XstarCfg<T, R>;
+    constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, NWY = C::NWY;
+    constexpr int STAGES = C::STAGES;
+
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    T* tiles = reinterpret_cast<T*>(base);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(STAGES) * C::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    volatile int32_t* stage_item = reinterpret_cast<int32_t*>(empty + STAGES);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWY);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NWY) {
+        // ------------------------------------------------------------ producer (star_kernels.cuh)
+        if (lane == 0) {
+            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                      iz = interior ? int(a.g.order0) : 0;
+            const CUtensorMap* own = interior ? &tm_int : &tm_src;
+            prefetch_tmap(own);
+            uint32_t it = 0;
+            while (true) {
+                const int item = atomicAdd(a.work_counter, 1);
+                if (item >= a.n_items) break;
+                int tx, ty, tz;
+                decode_item(a, item, tx, ty, tz);
+                const int x0 = a.x0base + tx * BX;
+                const int y0 = a.box.lo1 + ty * BY;
+                const int z0 = a.zs[2 * tz];
+                const int z1 = a.zs[2 * tz + 1];
+                const int c0 = int(a.g.lead) + x0 - RA - ix;
+                const int c1 = y0 + int(a.g.order) - R - iy;
+                for (int q = z0 - R; q < z1 + R; ++q, ++it) {
+                    const uint32_t s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                    stage_item[s] = item;
+                    mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
+                    tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+                }
+            }
+            const uint32_t s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+            stage_item[s] = -1;
+            mbar_arrive(&full[s]);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int xl = lane * VEC;
+    const int jr = warp;  // this warp's output row inside the tile
+    double zneg[R][VEC];  // centre values of the previous R planes (f64), ring by plane
+    double part[R][VEC];  // partial sums of the last R outputs, waiting for their d0+ taps
+    T chk = T(0);
+    uint32_t it = 0;
+    const int64_t pitch = a.g.pitch, plane = a.g.plane;
+
+    while (true) {
+        mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
+        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
+        if (item < 0) break;
+        int tx, ty, tz;
+        decode_item(a, item, tx, ty, tz);
+        const int x0 = a.x0base + tx * BX;
+        const int y0 = a.box.lo1 + ty * BY;
+        const int z0 = a.zs[2 * tz];
+        const int z1 = a.zs[2 * tz + 1];
+        const int x = x0 + xl;
+        const int y = y0 + jr;
+        const int nq = (z1 - z0) + 2 * R;
+        const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
+        const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
+        const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
+        T* const dst0 = a.dst + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+
+        // plane qi = q - (z0 - R) lives in ring slot qi mod R: unrolled by R, slots are static
+        for (int qb = 0; qb < nq; qb += R) {
+#pragma unroll
+            for (int p = 0; p < R; ++p) {
+                const int qi = qb + p;
+                if (qi < nq) {
+                    const int q = z0 - R + qi;
+                    const uint32_t s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1u);
+                    const T* t = tiles + size_t(s) * C::HALO_ELEMS;
+                    // the centre row of this warp with its x-halo, in f64
+                    double xr[VEC + 2 * RA];
+                    {
+                        T raw[VEC + 2 * RA];
+                        const T* row = t + (jr + R) * SW + xl;
+#pragma unroll
+                        for (int k = 0; k < (VEC + 2 * RA) / VEC; ++k) lds16(row + k * VEC, &raw[k * VEC]);
+#pragma unroll
+                        for (int k = 0; k < VEC + 2 * RA; ++k) xr[k] = double(raw[k]);
+                    }
+                    double acc[VEC];
+                    const bool q_out = q >= z0 && q < z1;
+                    if (q_out) {
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc[i] = xmul(xc.c0, xr[RA + i]);
+#pragma unroll
+                        for (int m = R; m >= 1; --m)  // (-m, 0, 0): plane q - m, slot (p - m) mod R
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i)
+                                acc[i] = xadd(acc[i], xmul(xc.cm[0][m - 1], zneg[(p - m + R) % R][i]));
+#pragma unroll
+                        for (int m = R; m >= 1; --m) {  // (0, -m, 0)
+                            T yv[VEC];
+                            lds16(t + (jr + R - m) * SW + xl + RA, yv);
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cm[1][m - 1], double(yv[i])));
+                        }
+#pragma unroll
+                        for (int m = R; m >= 1; --m)  // (0, 0, -m)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cm[2][m - 1], xr[RA + i - m]));
+#pragma unroll
+                        for (int m = 1; m <= R; ++m)  // (0, 0, +m)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cp[2][m - 1], xr[RA + i + m]));
+#pragma unroll
+                        for (int m = 1; m <= R; ++m) {  // (0, +m, 0)
+                            T yv[VEC];
+                            lds16(t + (jr + R + m) * SW + xl + RA, yv);
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cp[1][m - 1], double(yv[i])));
+                        }
+                    }
+                    __syncwarp();
+                    mbar_arrive_lane0(&empty[s], lane);  // every shared read of stage s is done
+                    ++it;
+                    // (+m, 0, 0): this plane is the +m tap of output q - m
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) {
+                        const int o = q - m;
+                        if (o >= z0 && o < z1)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i)
+                                part[(p - m + R) % R][i] =
+                                    xadd(part[(p - m + R) % R][i], xmul(xc.cp[0][m - 1], xr[RA + i]));
+                    }
+                    // output q - R is complete (it shares slot p with output q)
+                    const int z = q - R;
+                    if (z >= z0 && z < z1) {
+                        T outv[VEC];
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) {
+                            const double v = DIV ? __ddiv_rn(part[p][i], xc.divisor) : part[p][i];
+                            outv[i] = T(v);  // one rounding to the grid dtype (round to nearest even)
+                            chk = fma_t(T(0), outv[i], chk);
+                        }
+                        T* const dz = dst0 + (int64_t(z) + a.g.order0) * plane;
+                        if (y_in && x_full) stg16(dz, outv);
+                        else if (y_in && x_any)
+                            store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
+                                                a.box.hi2);
+                    }
+                    if (q_out)
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) part[p][i] = acc[i];
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) zneg[p][i] = xr[RA + i];
+                }
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, chk != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
+}
+
+template <typename T, int R, bool DIV>
+cudaError_t launch_exact_cfg(const StarLaunch& L, StarArgs<T> a, const XstarCoef& xc, const CUtensorMap* maps,
+                             cudaStream_t stream) {
+    using C = XstarCfg<T, R>;
+    auto kern = star_exact_kernel<T, R, DIV>;
+    if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
+    static uint64_t attr_devices = 0;
+    if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
+    a.n_tx = (a.box.hi2 - a.x0base + C::BX - 1) / C::BX;
+    a.n_ty = (a.box.hi1 - a.box.lo1 + C::BY - 1) / C::BY;
+    const int n0 = a.box.hi0 - a.box.lo0;
+    const int tiles = a.n_tx * a.n_ty;
+    const int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
+    int ntz;
+    a.lz = L.lz > 0 ? L.lz : choose_lz(n0, tiles, ctas, R, &ntz);
+    if (L.lz <= 0 && ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
+    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper, a.zs, 0);
+    a.n_signal = 0;
+    a.band_rows = 0;
+    if (L.band_pct > 0 && a.n_tx > 0) {
+        const int rows = std::max(1, (ctas * L.band_pct / 100) / a.n_tx);
+        if (rows < a.n_ty) a.band_rows = rows;
+    }
+    a.n_items = tiles * a.n_tz;
+    a.n_steps = 1;
+    if (a.n_items <= 0) return cudaSuccess;
+    const int grid = a.n_items < ctas ? a.n_items : ctas;
+    cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], a, xc);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_exact_t(const StarLaunch& L, const StarArgs<T>& a, const XstarCoef& xc, const CUtensorMap* maps,
+                           cudaStream_t s) {
+    const bool div = xc.divisor != 0.0;
+    switch (L.radius) {
+        case 1: return div ? launch_exact_cfg<T, 1, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 1, false>(L, a, xc, maps, s);
+        case 2: return div ? launch_exact_cfg<T, 2, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 2, false>(L, a, xc, maps, s);
+        case 3: return div ? launch_exact_cfg<T, 3, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 3, false>(L, a, xc, maps, s);
+        case 4: return div ? launch_exact_cfg<T, 4, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 4, false>(L, a, xc, maps, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace stkb

@@ -10,6 +10,13 @@ here the update expression is expanded into a polynomial over grid reads
   WAVE  w[0] = a*u[0] + b*p[0] + k[0] * (sum_k c_k * u[o_k])
   BOX   v[0] = (sum over the dense (2R+1)^3 cube) [/ d]   box / "other", R <= 2
 
+With ``precision="exact"`` a 3-D map whose update is literally the corpus star
+(corpus.py:77-120: ``c0*u.at(0,0,0) + c1*u.at(o1) + ...`` left-associated, every star
+offset once, the centre first and the rest sorted, optionally ``/ D``) matches
+
+  XSTAR the same float64 operations in the same order on the exact streaming kernel
+        (csrc/star_exact.cuh): bit-identical to run_target at streaming speed
+
 Everything else — larger box/"other" shapes, several updates, 2-D maps,
 in-place Jacobi updates, offset destinations, or ``precision="exact"`` —
 compiles to EXPR bytecode, which the device evaluates in float64 in parse
@@ -146,9 +153,12 @@ def match_map(bmap, *, exact: bool = False) -> MapPlan:
     params = dict(bmap.grid_args)  # kernel grid param -> module grid
     box = map_box(bmap)
     if exact:
-        p = compile_expr(bmap)
-        p.box, p.reason = box, "precision='exact'"
-        return p
+        try:
+            return match_exact_star(bmap, params, box)
+        except MatchError as why:
+            p = compile_expr(bmap)
+            p.box, p.reason = box, f"precision='exact': {why}"
+            return p
     try:
         return _match_fast(bmap, params, box)
     except MatchError as why:
@@ -280,6 +290,78 @@ def _match_fast(bmap, params: dict, box: tuple) -> MapPlan:
     for o, v in lap.items():
         coef[coef_index(o, r)] = v
     return MapPlan("wave", r, src, dst, prev=prev, vel=vel, coef=coef, wave_a=a_coef, wave_b=b_coef, box=box)
+
+
+def _const_value(n):
+    """A literal constant (negation of a literal folds exactly)."""
+    k = node_kind(n)
+    if k == "Const":
+        return float(n.value)
+    if k == "Unary" and node_kind(n.operand) == "Const":
+        return -float(n.operand.value)
+    return None
+
+
+def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
+    """XSTAR: the update is the canonical weighted star sum, term by term (executor.py's
+    evaluation: each ``c * u`` one float64 multiply, each ``+`` one float64 add, the
+    optional ``/ D`` one float64 division, then one rounding)."""
+    params = params if params is not None else dict(bmap.grid_args)
+    kern = bmap.kernel
+    if len(kern.updates) != 1 or kern.locals:
+        raise MatchError("not a single update without locals")
+    upd = kern.updates[0]
+    dims = len(upd.offset)
+    if dims != 3:
+        raise MatchError("the exact streaming kernel is 3-D")
+    if any(upd.offset):
+        raise MatchError("destination offset is not the centre")
+    expr = upd.expr
+    divisor = 0.0
+    if node_kind(expr) == "Binary" and expr.op == "/":
+        d = _const_value(expr.right)
+        if d is None or d == 0.0:
+            raise MatchError("division by something other than a non-zero literal")
+        divisor, expr = d, expr.left
+    terms = []
+    while node_kind(expr) == "Binary" and expr.op == "+":
+        terms.append(expr.right)
+        expr = expr.left
+    terms.append(expr)
+    terms.reverse()
+    coefs, offs, grids = [], [], set()
+    for t in terms:
+        if node_kind(t) != "Binary" or t.op != "*":
+            raise MatchError("a term is not coefficient * read")
+        c, rd = _const_value(t.left), t.right
+        if c is None:
+            c, rd = _const_value(t.right), t.left
+        if c is None or node_kind(rd) != "Read":
+            raise MatchError("a term is not coefficient * read")
+        coefs.append(c)
+        offs.append(tuple(rd.offset))
+        grids.add(rd.grid)
+    if len(grids) != 1:
+        raise MatchError("terms read several grids")
+    r = max(max(abs(v) for v in o) for o in offs)
+    if r < 1 or r > MAX_FAST_RADIUS:
+        raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
+    star = [(0, 0, 0)]
+    for axis in range(3):
+        for m in range(1, r + 1):
+            for sgn in (-1, 1):
+                o = [0, 0, 0]
+                o[axis] = sgn * m
+                star.append(tuple(o))
+    if offs != [star[0]] + sorted(star[1:]):
+        raise MatchError("terms are not the full star in corpus order (centre, then sorted offsets)")
+    src, dst = params[grids.pop()], params[upd.dest]
+    if src == dst:
+        raise MatchError("in-place update (reads and writes the same grid)")
+    coef = [0.0] * (6 * r + 1)
+    for o, c in zip(offs, coefs):
+        coef[coef_index(o, r)] = c
+    return MapPlan("xstar", r, src, dst, coef=coef, divisor=divisor, box=box)
 
 
 # ---------------------------------------------------------------------------

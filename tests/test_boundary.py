@@ -15,7 +15,7 @@ import pytest
 from conftest import ROOT, build_case, golden_cases, load_golden
 from paper_2309_04671_b200 import _lib as L
 from paper_2309_04671_b200 import corpus
-from paper_2309_04671_b200.matcher import coef_index, compile_expr, match_map
+from paper_2309_04671_b200.matcher import coef_index, compile_expr, map_box, match_map
 from paper_2309_04671_b200 import PlanError, plan_gpu
 
 
@@ -153,7 +153,8 @@ def test_device_bytecode_semantics_bitwise(case):
                 for _ in range(s.count):
                     run(s.body)
             else:
-                plan = match_map(s, exact=True)
+                plan = compile_expr(s)
+                plan.box = map_box(s)
                 emulate_bytecode(plan, state, s)
 
     run(bound.stmts)
@@ -196,3 +197,81 @@ def test_dead_inputs_detected():
     assert not halo_is_zero(g)
     g.data[0, 3, 3] = 0.0
     assert halo_is_zero(g)
+
+
+def emulate_xstar(plan, state):
+    """CPU model of star_exact.cuh's evaluation order, in float64 with one rounding:
+    centre, d0-negative (m = R..1), d1-negative, d2-negative, d2-positive (m = 1..R),
+    d1-positive, d0-positive, then the division."""
+    src, dst = state[plan.src], state[plan.dst]
+    R, o = plan.radius, src.order
+    u = src.data.astype(np.float64)
+    box = plan.box
+    n = tuple(hi - lo for lo, hi in box)
+
+    def tap(off):
+        return u[tuple(slice(o + lo + q, o + lo + q + e) for (lo, _), q, e in zip(box, off, n))]
+
+    def c(off):
+        return plan.coef[coef_index(off, R)]
+
+    def axis_off(ax, m):
+        v = [0, 0, 0]
+        v[ax] = m
+        return tuple(v)
+
+    acc = c((0, 0, 0)) * tap((0, 0, 0))
+    order = ([axis_off(0, -m) for m in range(R, 0, -1)] + [axis_off(1, -m) for m in range(R, 0, -1)] +
+             [axis_off(2, -m) for m in range(R, 0, -1)] + [axis_off(2, m) for m in range(1, R + 1)] +
+             [axis_off(1, m) for m in range(1, R + 1)] + [axis_off(0, m) for m in range(1, R + 1)])
+    for off in order:
+        acc = acc + c(off) * tap(off)
+    if plan.divisor:
+        acc = acc / plan.divisor
+    dst.data[tuple(slice(dst.order + lo, dst.order + hi) for lo, hi in box)] = acc.astype(dst.data.dtype)
+
+
+@pytest.mark.parametrize("case", ["star3d1r_12", "star3d2r_12", "star3d3r_10x12x14", "star3d4r_16", "star3d4r_f64",
+                                  "star3d4r_norm_16", "jacobi7_16", "star3d4r_w2_cross", "star3d4r_w3_slab7"])
+def test_exact_star_kernel_order_bitwise(case):
+    """precision='exact' routes the corpus stars (and c2's Jacobi-7, the normalised stars)
+    to the exact streaming kernel; its evaluation order, modelled here, reproduces the
+    reference's outputs bit for bit."""
+    meta, _, _, ins, outs = load_golden(case)
+    bound = build_case(meta)
+    state = {n: b.copy() for n, b in ins.items()}
+
+    def run(stmts):
+        for s in stmts:
+            k = type(s).__name__
+            if k == "BoundSwap":
+                state[s.first], state[s.second] = state[s.second], state[s.first]
+            elif k == "BoundFor":
+                for _ in range(s.count):
+                    run(s.body)
+            else:
+                plan = match_map(s, exact=True)
+                assert plan.kind == "xstar", plan.reason
+                emulate_xstar(plan, state)
+
+    run(bound.stmts)
+    for n, ref in outs.items():
+        assert np.array_equal(state[n].data, ref.data), n
+
+
+def test_exact_star_refuses_other_orders():
+    """Any other term order, a missing tap or a local goes to the bytecode kernel."""
+    import dataclasses
+
+    bound, _ = corpus.config_target("star3d1r", (8, 8, 8), 1)
+    m = next(_maps(bound.stmts))
+    assert match_map(m, exact=True).kind == "xstar"
+    e = m.kernel.updates[0].expr  # ((... + t5) + t6): swap the last two terms
+    swapped = dataclasses.replace(e, left=dataclasses.replace(e.left, right=e.right), right=e.left.right)
+    k2 = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=swapped),))
+    p = match_map(dataclasses.replace(m, kernel=k2), exact=True)
+    assert p.kind == "expr" and "corpus order" in p.reason
+    short = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=e.left),))
+    assert match_map(dataclasses.replace(m, kernel=short), exact=True).kind == "expr"
+    wave, _ = corpus.config_target("wave", (8, 8, 8), 1)
+    assert match_map(next(_maps(wave.stmts)), exact=True).kind == "expr"

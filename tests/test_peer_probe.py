@@ -26,5 +26,6 @@ def test_probe_timeout_is_a_failure(monkeypatch):
         raise subprocess.TimeoutExpired(cmd="probe", timeout=1)
 
     monkeypatch.setattr(subprocess, "run", boom)
+    monkeypatch.setattr(peer_probe, "_VERDICTS", {})  # verdicts are cached per device pair
     ok, why = peer_probe.probe(0, 1, timeout=1)
     assert ok is False and "did not finish" in why

@@ -1,0 +1,29 @@
+"""Time precision='exact' on one configuration (development tool).
+
+    python tools/exact_profile.py star3d4r_norm 512,512,512 f32 8
+Canonical stars run on the exact streaming kernel (XSTAR), other maps on the bytecode kernel.
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import bench  # noqa: E402
+from paper_2309_04671_b200 import DeviceTarget, corpus  # noqa: E402
+
+builder = sys.argv[1] if len(sys.argv) > 1 else "star3d4r_norm"
+shape = tuple(int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "512,512,512").split(","))
+dtype = sys.argv[3] if len(sys.argv) > 3 else "f32"
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 4
+bound, decls = corpus.config_target(builder, shape, steps, dtype)
+names = list(decls)
+dt = DeviceTarget({n: bench._decl_grid(d) for n, d in decls.items()}, names, precision="exact")
+bench.fill_device(dt, names, shape, builder)
+dt.set_program(bound.stmts[0].body)
+dt.run(2)
+dt.run(4)  # the CUDA graph of the step program is captured here, outside the timed run
+dt.sync()
+dt.run(steps)
+dt.sync()
+ms = dt.elapsed_ms() / steps
+n = shape[0] * shape[1] * shape[2]
+print(builder, dtype, dt.plans[0].kind, round(ms, 3), "ms/step", round(n / ms / 1e6, 1), "GPts/s")

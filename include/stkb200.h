@@ -169,6 +169,9 @@ int stkb_run_once(stkb_domain *dom);             /* one step, direct launches (n
 int stkb_sync(stkb_domain *dom);
 int stkb_elapsed_ms(stkb_domain *dom, double *ms); /* device time of the last stkb_run */
 int stkb_launches(stkb_domain *dom, int64_t *count); /* kernels launched by the last stkb_run */
+/* how the last stkb_run executed: 0 = one launch per map and step (CUDA graphs), 1 = fused
+ * two-step sweeps (stkb_set_fused_steps), 2 = multi-step launches (stkb_set_multi_steps) */
+int stkb_run_mode(const stkb_domain *dom, int32_t *mode);
 int stkb_binding(const stkb_domain *dom, int32_t name, int32_t *buffer);
 int stkb_nonfinite(stkb_domain *dom, int32_t tag, int32_t *flag); /* sticky; clears it */
 

@@ -32,7 +32,7 @@ EXPORTS = (
     "stkb_download", "stkb_upload_async", "stkb_download_async", "stkb_upload_grid", "stkb_download_grid",
     "stkb_program_reset",
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
-    "stkb_elapsed_ms", "stkb_launches", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
+    "stkb_elapsed_ms", "stkb_launches", "stkb_run_mode", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
     "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
     "stkb_flags_ipc_handle", "stkb_buffer_ptr", "stkb_flags_ptr", "stkb_ipc_open", "stkb_ipc_close", "stkb_set_peer",
@@ -126,6 +126,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_sync": [V],
         "stkb_elapsed_ms": [V, P(dbl)],
         "stkb_launches": [V, P(i64)],
+        "stkb_run_mode": [V, P(i32)],
         "stkb_binding": [V, i32, P(i32)],
         "stkb_nonfinite": [V, i32, P(i32)],
         "stkb_run_target": [V, P(V), i64],

@@ -257,6 +257,12 @@ class DeviceTarget:
         L.call("stkb_launches", self.h, ctypes.byref(v))
         return v.value
 
+    def run_mode(self) -> str:
+        """How the last run executed: "single", "fused" (two-step sweeps) or "multi"."""
+        v = ctypes.c_int32()
+        L.call("stkb_run_mode", self.h, ctypes.byref(v))
+        return {0: "single", 1: "fused", 2: "multi"}.get(v.value, str(v.value))
+
     def check_finite(self) -> None:
         """Warn per map that produced non-finite values (executor.py:247-253)."""
         for tag, kname in self._tags.items():

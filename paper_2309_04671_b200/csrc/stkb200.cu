@@ -132,6 +132,7 @@ struct stkb_domain {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;
     int64_t last_launches = 0;
+    int32_t last_mode = 0;  // how the last stkb_run executed: 0 single steps, 1 fused sweeps, 2 multi-step
     int32_t* d_flags = nullptr;
     void* d_partials = nullptr;
     void* d_stage = nullptr;  // H2D staging: contiguous PCIe copies, then a repitch kernel
@@ -1152,6 +1153,7 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
         CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
         dom->timed = true;
         dom->last_launches = launches;
+        dom->last_mode = 2;
         return STKB_OK;
     }
     if (const MapOp* tb = steps >= 4 ? tb_map(dom) : nullptr) {
@@ -1227,6 +1229,7 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
         CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
         dom->timed = true;
         dom->last_launches = launches;
+        dom->last_mode = 1;
         return STKB_OK;
     }
     CUDA_TRY(cudaEventRecord(dom->ev0, dom->stream));
@@ -1270,6 +1273,7 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
     CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
     dom->timed = true;
     dom->last_launches = launches;
+    dom->last_mode = 0;
     return STKB_OK;
 }
 
@@ -1283,6 +1287,7 @@ int stkb_run_once(stkb_domain* dom) {
     CUDA_TRY(cudaEventRecord(dom->ev1, dom->stream));
     dom->timed = true;
     dom->last_launches = launches;
+    dom->last_mode = 0;
     return STKB_OK;
 }
 
@@ -1299,6 +1304,12 @@ int stkb_elapsed_ms(stkb_domain* dom, double* ms) {
     float f = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&f, dom->ev0, dom->ev1));
     *ms = f;
+    return STKB_OK;
+}
+
+int stkb_run_mode(const stkb_domain* dom, int32_t* mode) {
+    if (!dom || !mode) return fail(STKB_ERR_ARG, "null argument");
+    *mode = dom->last_mode;
     return STKB_OK;
 }
 

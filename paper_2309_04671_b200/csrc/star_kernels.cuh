@@ -437,40 +437,47 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                             for (int k = 0; k < NPK; ++k) cv[j][k] = K::make(&cvs[j][k * W]);
 
                         if (q >= z0 && q < z1) {
-                            // output q: its accumulator already holds the d0 taps of planes < q
+                            // output q: its accumulator already holds the d0 taps of planes < q.
+                            // The d2 taps run tap by tap across every (row, pack) of the thread, so
+                            // its TY x NPK accumulator chains interleave (same per-point order).
+                            T xr[TY][VEC + 2 * RA];  // left halo | centre | right halo of each row
     #pragma unroll
                             for (int j = 0; j < TY; ++j) {
-                                T xr[VEC + 2 * RA];  // left halo | centre | right halo of row j
                                 const T* row = t + (jr0 + j + R) * SW + xl;
     #pragma unroll
                                 for (int k = 0; k < RA / VEC; ++k) {
-                                    lds16(row + k * VEC, &xr[k * VEC]);
-                                    lds16(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
+                                    lds16(row + k * VEC, &xr[j][k * VEC]);
+                                    lds16(row + RA + VEC + k * VEC, &xr[j][RA + VEC + k * VEC]);
                                 }
     #pragma unroll
-                                for (int i = 0; i < VEC; ++i) xr[RA + i] = cvs[j][i];
+                                for (int i = 0; i < VEC; ++i) xr[j][RA + i] = cvs[j][i];
+                            }
     #pragma unroll
-                                for (int k = 0; k < NPK; ++k) {
-                                    P s_ = K::fma(a.c0, cv[j][k], acc[p][j][k]);
+                            for (int j = 0; j < TY; ++j)
     #pragma unroll
-                                    for (int m = 1; m <= R; ++m) {
+                                for (int k = 0; k < NPK; ++k) acc[p][j][k] = K::fma(a.c0, cv[j][k], acc[p][j][k]);
+    #pragma unroll
+                            for (int m = 1; m <= R; ++m) {
+    #pragma unroll
+                                for (int j = 0; j < TY; ++j)
+    #pragma unroll
+                                    for (int k = 0; k < NPK; ++k) {
+                                        P s_ = acc[p][j][k];
                                         if (W == 1 || (m % 2) == 0 || !ODD_SCALAR) {
-                                            s_ = K::fma(a.cm[2][m - 1], K::make(&xr[RA + k * W - m]), s_);
-                                            s_ = K::fma(a.cp[2][m - 1], K::make(&xr[RA + k * W + m]), s_);
+                                            s_ = K::fma(a.cm[2][m - 1], K::make(&xr[j][RA + k * W - m]), s_);
+                                            s_ = K::fma(a.cp[2][m - 1], K::make(&xr[j][RA + k * W + m]), s_);
                                         } else {  // odd shift: the pair straddles two register pairs
-                                            T l[W], r[W];
+                                            T l[W];
                                             K::put(l, s_);
     #pragma unroll
                                             for (int w = 0; w < W; ++w) {
-                                                l[w] = fma_t(a.cm[2][m - 1], xr[RA + k * W + w - m], l[w]);
-                                                l[w] = fma_t(a.cp[2][m - 1], xr[RA + k * W + w + m], l[w]);
+                                                l[w] = fma_t(a.cm[2][m - 1], xr[j][RA + k * W + w - m], l[w]);
+                                                l[w] = fma_t(a.cp[2][m - 1], xr[j][RA + k * W + w + m], l[w]);
                                             }
-                                            (void)r;
                                             s_ = K::make(l);
                                         }
+                                        acc[p][j][k] = s_;
                                     }
-                                    acc[p][j][k] = s_;
-                                }
                             }
                             // d1 (y) taps: stream the TY+2R rows of this warp's column
     #pragma unroll

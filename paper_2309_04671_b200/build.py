@@ -22,6 +22,8 @@ HEADERS = ["common.cuh", "star_kernels.cuh", "star_tb.cuh", "star_exact.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"),
          f"-DSTKB_VARIANTS={int(os.environ.get('STKB_BUILD_VARIANTS', '1'))}"]
+if os.environ.get("STKB_BUILD_MAX_STAGES"):  # experiments: deeper TMA rings
+    FLAGS.append(f"-DSTKB_MAX_STAGES={int(os.environ['STKB_BUILD_MAX_STAGES'])}")
 
 
 def nvcc() -> str:

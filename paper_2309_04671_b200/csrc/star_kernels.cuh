@@ -55,7 +55,10 @@ struct StarCfg {
     static constexpr uint32_t CTR_BYTES = CTR_ELEMS * sizeof(T);
     static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * sizeof(T);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+#ifndef STKB_MAX_STAGES
+#define STKB_MAX_STAGES 8
+#endif
+    static constexpr int STAGES = STAGES_RAW > STKB_MAX_STAGES ? STKB_MAX_STAGES : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
     static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
                                    STAGES * sizeof(int32_t);
     static constexpr int THREADS = (NWY + 1) * 32;

@@ -27,7 +27,22 @@
 
 #include "star_kernels.cuh"
 
+// 1 (measured slower, not the default): each warp computes v on its own output rows only (plus the tile's halo rows on the first /
+// last warp) and takes the neighbouring rows its stage 2 needs from the adjacent warps through
+// shared memory (one consumer barrier per plane); 0: every warp recomputes its R halo rows
+#ifndef STKB_TB_XCH
+#define STKB_TB_XCH 0
+#endif
+
 namespace stkb {
+
+__device__ __forceinline__ void sts16(float* p, const float* v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]) : "memory");
+}
+__device__ __forceinline__ void sts16(double* p, const double* v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(p)), "d"(v[0]), "d"(v[1]) : "memory");
+}
 
 template <typename T, int R, int TY2, int NW>
 struct TbCfg {
@@ -46,13 +61,18 @@ struct TbCfg {
     static constexpr uint32_t HALO_BYTES = SW * SH * sizeof(T);
     static constexpr uint32_t V_BYTES = VW * VH * sizeof(T);
     static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * sizeof(T);
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+    // v-row exchange (STKB_TB_XCH): each warp publishes its first and last R v rows per
+    // plane, double-buffered by plane parity
+    static constexpr int XROW = 32 * VEC;  // one v row of the tile
+    static constexpr uint32_t XBUF_BYTES = STKB_TB_XCH ? 2u * NW * 2 * R * XROW * sizeof(T) : 0u;
+    static constexpr int STAGES_RAW = (200 * 1024 - int(XBUF_BYTES)) / STAGE_BYTES;
     // a power of two: the stage index and phase of plane `it` are a mask and a shift
     static constexpr int STAGES = STAGES_RAW >= 8 ? 8 : (STAGES_RAW >= 4 ? 4 : 2);
     static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
-                                   STAGES * sizeof(int32_t);
+                                   STAGES * sizeof(int32_t) + 16 + XBUF_BYTES;
     static constexpr int THREADS = (NW + 1) * 32;
     static_assert(SW <= 256 && SH <= 256, "TMA box dims are limited to 256");
+    static_assert(!STKB_TB_XCH || TY2 >= R, "the exchange needs R own rows per warp");
 };
 
 template <typename T, int R, int TY2, int NW, bool DIV>
@@ -72,6 +92,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(STAGES) * C::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     volatile int32_t* stage_item = reinterpret_cast<int32_t*>(empty + STAGES);
+    T* xbuf = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(stage_item + STAGES) + 15) & ~uintptr_t(15));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -165,6 +186,15 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
     uint32_t it = 0;
     const int64_t pitch = a.g.pitch, plane = a.g.plane;
     const bool need_v = *reinterpret_cast<const volatile int32_t*>(frozen_nz) != 0;
+    // v row i (= tile row jr0 - R + i) is computed by this warp: its own rows, and the R halo
+    // rows above / below only on the first / last warp (with the exchange; warp-uniform)
+    const bool top = warp == 0, bot = warp == NW - 1;
+    auto row_on = [&](int i) -> bool {
+        return !STKB_TB_XCH || (i >= R && i < R + TY2) || (i < R && top) || (i >= R + TY2 && bot);
+    };
+    // u tile rows (relative to jr0) the active v rows read: [first, last]
+    const int rr_first = STKB_TB_XCH && !top ? R : 0;
+    const int rr_last = STKB_TB_XCH && !bot ? TY2 + 3 * R - 1 : TY1 + 2 * R - 1;
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
@@ -210,6 +240,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                     if (q >= z0 - R && q < z1 + R) {
 #pragma unroll
                         for (int j = 0; j < TY1; ++j) {
+                            if (!row_on(j)) continue;
                             T xr[VEC + 2 * RA];
                             const T* row = t + (jr0 + j + R) * SW + xl;
                             lds16(row, &xr[0]);
@@ -244,20 +275,20 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
 #pragma unroll
                                 for (int j = 0; j < TY1; ++j) {
                                     const int m = rr - (j + R);
-                                    if (m != 0 && m >= -R && m <= R) {
+                                    if (m != 0 && m >= -R && m <= R && row_on(j)) {
                                         const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
 #pragma unroll
                                         for (int k = 0; k < NPK; ++k)
                                             acc1[p][j][k] = K::fma(c, cv[rr - R][k], acc1[p][j][k]);
                                     }
                                 }
-                            } else {
+                            } else if (rr >= rr_first && rr <= rr_last) {
                                 T yv_[VEC];
                                 lds16(t + (jr0 + rr) * SW + xl + RA, yv_);
 #pragma unroll
                                 for (int j = 0; j < TY1; ++j) {
                                     const int m = rr - (j + R);
-                                    if (m >= -R && m <= R) {
+                                    if (m >= -R && m <= R && row_on(j)) {
                                         const T c = m < 0 ? a.cm[1][-m - 1] : a.cp[1][m - 1];
 #pragma unroll
                                         for (int k = 0; k < NPK; ++k)
@@ -270,6 +301,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                     if (q < z1 + R) {
 #pragma unroll
                         for (int j = 0; j < TY1; ++j)
+                            if (row_on(j))
 #pragma unroll
                             for (int k = 0; k < NPK; ++k) {
                                 acc1[(p + R) % NS][j][k] = K::mul(a.cm[0][R - 1], cv[j][k]);
@@ -280,6 +312,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                     }
 #pragma unroll
                     for (int j = 0; j < TY1; ++j)
+                        if (row_on(j))
 #pragma unroll
                         for (int k = 0; k < NPK; ++k)
 #pragma unroll
@@ -312,6 +345,7 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                             const T* vt = t + C::U_ELEMS + jr0 * C::VW + xl;
 #pragma unroll
                             for (int j = 0; j < TY1; ++j) {
+                                if (!row_on(j)) continue;
                                 const int y = yv + j;
                                 const bool row_in = z_in && y >= a.box.lo1 && y < a.box.hi1;
                                 T fz[VEC] = {};
@@ -325,6 +359,24 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
                             }
                         }
 
+                        if constexpr (STKB_TB_XCH) {
+                            // publish this warp's first / last R v rows, take the neighbours'
+                            T* xb = xbuf + (qv & 1) * (NW * 2 * R * C::XROW);
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+                                sts16(xb + ((warp * 2 + 0) * R + r) * C::XROW + xl, vv[R + r]);
+                                sts16(xb + ((warp * 2 + 1) * R + r) * C::XROW + xl, vv[TY2 + r]);
+                            }
+                            asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+                            if (!top)
+#pragma unroll
+                                for (int r = 0; r < R; ++r)
+                                    lds16(xb + (((warp - 1) * 2 + 1) * R + r) * C::XROW + xl, vv[r]);
+                            if (!bot)
+#pragma unroll
+                                for (int r = 0; r < R; ++r)
+                                    lds16(xb + (((warp + 1) * 2 + 0) * R + r) * C::XROW + xl, vv[R + TY2 + r]);
+                        }
                         // -------- stage 2: v plane qv -> u(t+2)
                         P cw[TY2][NPK];
 #pragma unroll

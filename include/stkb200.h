@@ -55,6 +55,10 @@ extern "C" {
                             float64 with the terms in the corpus order (centre, then the star
                             offsets sorted), one rounding per store: bit-identical to run_target
                             at streaming speed; 3-D, radius 1..4, coef layout as STAR */
+#define STKB_MAP_XWAVE 6 /* exact acoustic wave: dst = (wave_a*src[0] - prev[0]) + vel[0] * (coef[0]*src[0]
+                            + coef[1]*S_1 + ... + coef[R]*S_R), S_m = the six +-m axis taps of src summed
+                            d0-, d0+, d1-, d1+, d2-, d2+; float64 in that order, one rounding per store
+                            (the c3 program as run_target evaluates it); 3-D, radius 1..4 */
 
 /* step-program execution precision for STAR/WAVE maps */
 #define STKB_PREC_FAST 0 /* accumulate in the grid dtype with FMA (tolerance-checked) */

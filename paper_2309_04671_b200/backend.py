@@ -309,12 +309,12 @@ def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = No
     bx = box if box is not None else plan.box
     for i, (lo, hi) in enumerate(bx):
         d.lo[i], d.hi[i] = lo, hi
-    if plan.kind in ("star", "wave", "box", "xstar"):
+    if plan.kind in ("star", "wave", "box", "xstar", "xwave"):
         d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX,
-                  "xstar": L.STKB_MAP_XSTAR}[plan.kind]
+                  "xstar": L.STKB_MAP_XSTAR, "xwave": L.STKB_MAP_XWAVE}[plan.kind]
         d.radius = plan.radius
         d.src, d.dst = index[plan.src], index[plan.dst]
-        if plan.kind == "wave":
+        if plan.kind in ("wave", "xwave"):
             d.prev, d.vel = index[plan.prev], index[plan.vel]
             d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
         if plan.kind == "box" and len(plan.coef) > 125:  # 3-D box of radius 3..4

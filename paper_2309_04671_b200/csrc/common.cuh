@@ -98,6 +98,13 @@ struct XstarCoef {
     double divisor;   // 0: none, else the sum is divided by it (IEEE division, as numpy does)
 };
 
+// coefficients of the exact wave kernel (star_exact.cuh): a*u - p + k*(c0*u + sum_m l[m-1]*S_m)
+struct XwaveCoef {
+    double a;
+    double c0;
+    double l[4];
+};
+
 // ---------------------------------------------------------------------------
 // mbarrier / TMA PTX wrappers (sm_90+ ISA, used here for sm_100a)
 
@@ -252,4 +259,6 @@ cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cuda
 cudaError_t launch_exact_f32(const StarLaunch& L, const StarArgs<float>& a, const XstarCoef& xc, cudaStream_t s);
 cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, const XstarCoef& xc, cudaStream_t s);
 int exact_tile(int dtype, int radius, int* bx, int* by, int* halo_x);
+cudaError_t launch_xwave_f32(const StarLaunch& L, const StarArgs<float>& a, const XwaveCoef& xc, cudaStream_t s);
+cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, const XwaveCoef& xc, cudaStream_t s);
 }  // namespace stkb

@@ -11,6 +11,15 @@ cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, con
     return launch_exact_t<double>(L, a, xc, L.maps, s);
 }
 
+cudaError_t launch_xwave_f32(const StarLaunch& L, const StarArgs<float>& a, const XwaveCoef& xc, cudaStream_t s) {
+    return launch_xwave_t<float>(L, a, xc, L.maps, s);
+}
+
+cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, const XwaveCoef& xc, cudaStream_t s) {
+    return launch_xwave_t<double>(L, a, xc, L.maps, s);
+}
+
+// exact star and exact wave share the tile shape (one output row per warp, 15 warps)
 int exact_tile(int dtype, int radius, int* bx, int* by, int* halo_x) {
     if (radius < 1 || radius > 4) return 1;
     if (dtype == 1) {

@@ -234,6 +234,237 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
     if (__any_sync(0xffffffffu, chk != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Exact acoustic wave: the c3 program of SURVEY.md §8(d) as the reference parses it,
+//     up.at(0,0,0).set(A*u.at(0,0,0) - up.at(0,0,0) + kap.at(0,0,0) * (C0*u.at(0,0,0)
+//                      + L1*(S_1) + ... + LR*(S_R)))
+//     S_m = u(-m,0,0) + u(m,0,0) + u(0,-m,0) + u(0,m,0) + u(0,0,-m) + u(0,0,m)  (left to right)
+// evaluated node by node in float64 (executor.py:81-106) and rounded once.  Each ring sum
+// starts with BOTH d0 taps, so output o can only be evaluated once plane o+R has arrived and
+// every in-plane tap is still needed: the 2R+1 planes o-R..o+R stay in the shared ring (a
+// plane is released after the last output that reads it), and output o is computed from
+// shared memory alone when plane o+R lands.  u_prev and kappa are read from global memory.
+template <typename T, int R>
+struct XwaveCfg {
+    static constexpr int VEC = 16 / sizeof(T);
+    static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
+    static constexpr int NWY = 15;
+    static constexpr int BX = 32 * VEC;
+    static constexpr int BY = NWY;
+    static constexpr int SW = BX + 2 * RA;
+    static constexpr int SH = BY + 2 * R;
+    static constexpr int HALO_ELEMS = ((SW * SH * int(sizeof(T)) + 127) / 128) * 128 / int(sizeof(T));
+    static constexpr uint32_t HALO_BYTES = SW * SH * sizeof(T);
+    static constexpr uint32_t STAGE_BYTES = HALO_ELEMS * sizeof(T);
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 2 * R + 4 ? 2 * R + 4 : STAGES_RAW;
+    static_assert(STAGES >= 2 * R + 2, "the exact wave keeps 2R+1 planes resident plus one in flight");
+    static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
+                                   STAGES * sizeof(int32_t);
+    static constexpr int THREADS = (NWY + 1) * 32;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__((XwaveCfg<T, R>::NWY + 1) * 32, 1)
+wave_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
+                  const __grid_constant__ StarArgs<T> a, const __grid_constant__ XwaveCoef xc) {
+    using C = XwaveCfg<T, R>;
+    constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, NWY = C::NWY;
+    constexpr int STAGES = C::STAGES;
+
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    T* tiles = reinterpret_cast<T*>(base);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(STAGES) * C::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    volatile int32_t* stage_item = reinterpret_cast<int32_t*>(empty + STAGES);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWY);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NWY) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                      iz = interior ? int(a.g.order0) : 0;
+            const CUtensorMap* own = interior ? &tm_int : &tm_src;
+            prefetch_tmap(own);
+            uint32_t it = 0;
+            while (true) {
+                const int item = atomicAdd(a.work_counter, 1);
+                if (item >= a.n_items) break;
+                int tx, ty, tz;
+                decode_item(a, item, tx, ty, tz);
+                const int x0 = a.x0base + tx * BX;
+                const int y0 = a.box.lo1 + ty * BY;
+                const int z0 = a.zs[2 * tz];
+                const int z1 = a.zs[2 * tz + 1];
+                const int c0 = int(a.g.lead) + x0 - RA - ix;
+                const int c1 = y0 + int(a.g.order) - R - iy;
+                for (int q = z0 - R; q < z1 + R; ++q, ++it) {
+                    const uint32_t s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                    stage_item[s] = item;
+                    mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
+                    tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+                }
+            }
+            const uint32_t s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+            stage_item[s] = -1;
+            mbar_arrive(&full[s]);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int xl = lane * VEC;
+    const int jr = warp;
+    T chk = T(0);
+    uint32_t it = 0;
+    const int64_t pitch = a.g.pitch, plane = a.g.plane;
+
+    while (true) {
+        mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
+        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
+        if (item < 0) break;
+        int tx, ty, tz;
+        decode_item(a, item, tx, ty, tz);
+        const int x0 = a.x0base + tx * BX;
+        const int y0 = a.box.lo1 + ty * BY;
+        const int z0 = a.zs[2 * tz];
+        const int z1 = a.zs[2 * tz + 1];
+        const int x = x0 + xl;
+        const int y = y0 + jr;
+        const int nq = (z1 - z0) + 2 * R;
+        const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
+        const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
+        const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
+        const int64_t row_off = (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+        const uint32_t it0 = it;
+        for (int qi = 0; qi < nq; ++qi) {
+            const uint32_t cur = it0 + qi;  // plane q = z0 - R + qi
+            mbar_wait(&full[cur % STAGES], (cur / STAGES) & 1u);
+            if (qi >= 2 * R) {
+                // output o = z0 + qi - 2R: planes o-R .. o+R are resident, plane o+d at cur - R + d
+                const int o = z0 + qi - 2 * R;
+                const int64_t off = (int64_t(o) + a.g.order0) * plane + row_off;
+                T pv[VEC] = {}, kv[VEC] = {};
+                if (y_in && x_any) {  // read early: the shared-memory work hides the latency
+                    load16(a.prev + off, pv);  // plain load: u_prev may be the destination (in place)
+                    ldg16(a.vel + off, kv);
+                }
+                const T* to = tiles + size_t((cur - R) % STAGES) * C::HALO_ELEMS;
+                double xr[VEC + 2 * RA];
+                {
+                    T raw[VEC + 2 * RA];
+                    const T* row = to + (jr + R) * SW + xl;
+#pragma unroll
+                    for (int k = 0; k < (VEC + 2 * RA) / VEC; ++k) lds16(row + k * VEC, &raw[k * VEC]);
+#pragma unroll
+                    for (int k = 0; k < VEC + 2 * RA; ++k) xr[k] = double(raw[k]);
+                }
+                double lap[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) lap[i] = xmul(xc.c0, xr[RA + i]);
+#pragma unroll
+                for (int m = 1; m <= R; ++m) {
+                    T zm[VEC], zp[VEC], ym[VEC], yp[VEC];
+                    lds16(tiles + size_t((cur - R - m) % STAGES) * C::HALO_ELEMS + (jr + R) * SW + xl + RA, zm);
+                    lds16(tiles + size_t((cur - R + m) % STAGES) * C::HALO_ELEMS + (jr + R) * SW + xl + RA, zp);
+                    lds16(to + (jr + R - m) * SW + xl + RA, ym);
+                    lds16(to + (jr + R + m) * SW + xl + RA, yp);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        double sm = xadd(double(zm[i]), double(zp[i]));
+                        sm = xadd(sm, double(ym[i]));
+                        sm = xadd(sm, double(yp[i]));
+                        sm = xadd(sm, xr[RA + i - m]);
+                        sm = xadd(sm, xr[RA + i + m]);
+                        lap[i] = xadd(lap[i], xmul(xc.l[m - 1], sm));
+                    }
+                }
+                T outv[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    const double head = __dsub_rn(xmul(xc.a, xr[RA + i]), double(pv[i]));
+                    outv[i] = T(xadd(head, xmul(double(kv[i]), lap[i])));
+                    chk = fma_t(T(0), outv[i], chk);
+                }
+                __syncwarp();
+                // plane o - R is read by no later output of this item
+                mbar_arrive_lane0(&empty[(cur - 2 * R) % STAGES], lane);
+                T* const dz = a.dst + off;
+                if (o >= a.box.lo0 && o < a.box.hi0 && y_in && x_full) stg16(dz, outv);
+                else if (o >= a.box.lo0 && o < a.box.hi0 && y_in && x_any)
+                    store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
+                                        a.box.hi2);
+            }
+        }
+        // the item's last 2R planes
+        __syncwarp();
+        for (int qi = nq - 2 * R; qi < nq; ++qi) mbar_arrive_lane0(&empty[(it0 + qi) % STAGES], lane);
+        it = it0 + nq;
+    }
+    if (__any_sync(0xffffffffu, chk != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
+}
+
+template <typename T, int R>
+cudaError_t launch_xwave_cfg(const StarLaunch& L, StarArgs<T> a, const XwaveCoef& xc, const CUtensorMap* maps,
+                             cudaStream_t stream) {
+    using C = XwaveCfg<T, R>;
+    auto kern = wave_exact_kernel<T, R>;
+    if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
+    static uint64_t attr_devices = 0;
+    if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
+    a.n_tx = (a.box.hi2 - a.x0base + C::BX - 1) / C::BX;
+    a.n_ty = (a.box.hi1 - a.box.lo1 + C::BY - 1) / C::BY;
+    const int n0 = a.box.hi0 - a.box.lo0;
+    const int tiles = a.n_tx * a.n_ty;
+    const int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
+    int ntz;
+    a.lz = L.lz > 0 ? L.lz : choose_lz(n0, tiles, ctas, R, &ntz);
+    if (L.lz <= 0 && ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
+    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper, a.zs, 0);
+    a.n_signal = 0;
+    a.band_rows = 0;
+    if (L.band_pct > 0 && a.n_tx > 0) {
+        const int rows = std::max(1, (ctas * L.band_pct / 100) / a.n_tx);
+        if (rows < a.n_ty) a.band_rows = rows;
+    }
+    a.n_items = tiles * a.n_tz;
+    a.n_steps = 1;
+    if (a.n_items <= 0) return cudaSuccess;
+    const int grid = a.n_items < ctas ? a.n_items : ctas;
+    cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], a, xc);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_xwave_t(const StarLaunch& L, const StarArgs<T>& a, const XwaveCoef& xc, const CUtensorMap* maps,
+                           cudaStream_t s) {
+    switch (L.radius) {
+        case 1: return launch_xwave_cfg<T, 1>(L, a, xc, maps, s);
+        case 2: return launch_xwave_cfg<T, 2>(L, a, xc, maps, s);
+        case 3: return launch_xwave_cfg<T, 3>(L, a, xc, maps, s);
+        case 4: return launch_xwave_cfg<T, 4>(L, a, xc, maps, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename T, int R, bool DIV>
 cudaError_t launch_exact_cfg(const StarLaunch& L, StarArgs<T> a, const XstarCoef& xc, const CUtensorMap* maps,
                              cudaStream_t stream) {

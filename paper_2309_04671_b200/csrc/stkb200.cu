@@ -388,7 +388,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     }
 
     int bx, by, hx;
-    if (d.kind == STKB_MAP_XSTAR) exact_tile(dom->desc.dtype, R, &bx, &by, &hx);
+    if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE) exact_tile(dom->desc.dtype, R, &bx, &by, &hx);
     else star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
 #ifdef STKB_EXP_NOYHALO
@@ -466,7 +466,15 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         L.step_counters = dom->d_multi;
     }
     cudaError_t e;
-    if (d.kind == STKB_MAP_XSTAR) {
+    if (d.kind == STKB_MAP_XWAVE) {
+        if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact wave maps launch over their box");
+        XwaveCoef xc{};
+        xc.a = d.wave_a;
+        xc.c0 = d.coef[0];
+        for (int m = 1; m <= R; ++m) xc.l[m - 1] = d.coef[m];
+        if constexpr (sizeof(T) == 4) e = launch_xwave_f32(L, a, xc, dom->stream);
+        else e = launch_xwave_f64(L, a, xc, dom->stream);
+    } else if (d.kind == STKB_MAP_XSTAR) {
         if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
         XstarCoef xc{};
         xc.c0 = d.coef[0];
@@ -987,8 +995,10 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     MapOp op;
     op.d = d;
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
-    if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX || d.kind == STKB_MAP_XSTAR) {
-        if (d.kind == STKB_MAP_XSTAR && nd != 3) return fail(STKB_ERR_UNSUPPORTED, "exact star maps are 3-D");
+    if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX || d.kind == STKB_MAP_XSTAR ||
+        d.kind == STKB_MAP_XWAVE) {
+        if ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE) && nd != 3)
+            return fail(STKB_ERR_UNSUPPORTED, "exact streaming maps are 3-D");
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
             return fail(STKB_ERR_UNSUPPORTED, nd == 1 ? "1-D maps run as EXPR maps" : "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
@@ -1004,7 +1014,7 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
         if (int rc = check_name(dom, d.src, "src")) return rc;
         if (int rc = check_name(dom, d.dst, "dst")) return rc;
         if (d.src == d.dst) return fail(STKB_ERR_ARG, "star map reads and writes the same grid (needs a snapshot: use EXPR)");
-        if (d.kind == STKB_MAP_WAVE) {
+        if (d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_XWAVE) {
             if (int rc = check_name(dom, d.prev, "prev")) return rc;
             if (int rc = check_name(dom, d.vel, "vel")) return rc;
             if (d.vel == d.dst) return fail(STKB_ERR_ARG, "wave map writes its velocity grid");
@@ -1372,7 +1382,8 @@ int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges
     }
     int items = 0;
     int rc = STKB_OK;
-    const bool streaming = op.d.kind != STKB_MAP_EXPR && op.d.kind != STKB_MAP_XSTAR && dom->desc.ndim == 3;
+    const bool streaming = op.d.kind != STKB_MAP_EXPR && op.d.kind != STKB_MAP_XSTAR && op.d.kind != STKB_MAP_XWAVE &&
+                           dom->desc.ndim == 3;
     if (streaming) {
         RangeSpec rs;
         rs.n = n_ranges;
@@ -1410,7 +1421,7 @@ int stkb_launch_map_pull(stkb_domain* dom, int32_t map_index) {
     dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     MapOp& op = dom->maps[map_index];
-    if (op.d.kind == STKB_MAP_EXPR || op.d.kind == STKB_MAP_XSTAR || dom->desc.ndim != 3)
+    if (op.d.kind == STKB_MAP_EXPR || op.d.kind == STKB_MAP_XSTAR || op.d.kind == STKB_MAP_XWAVE || dom->desc.ndim != 3)
         return fail(STKB_ERR_UNSUPPORTED, "the fused halo exchange needs a 3-D streaming map");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     return dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, RangeSpec(), true)

@@ -155,10 +155,13 @@ def match_map(bmap, *, exact: bool = False) -> MapPlan:
     if exact:
         try:
             return match_exact_star(bmap, params, box)
-        except MatchError as why:
-            p = compile_expr(bmap)
-            p.box, p.reason = box, f"precision='exact': {why}"
-            return p
+        except MatchError as why_star:
+            try:
+                return match_exact_wave(bmap, params, box)
+            except MatchError as why_wave:
+                p = compile_expr(bmap)
+                p.box, p.reason = box, f"precision='exact': {why_star}; {why_wave}"
+                return p
     try:
         return _match_fast(bmap, params, box)
     except MatchError as why:
@@ -362,6 +365,87 @@ def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> Ma
     for o, c in zip(offs, coefs):
         coef[coef_index(o, r)] = c
     return MapPlan("xstar", r, src, dst, coef=coef, divisor=divisor, box=box)
+
+
+def _chain(expr, op: str) -> list:
+    """Operands of a left-associated chain ((a op b) op c) ... in source order."""
+    out = []
+    while node_kind(expr) == "Binary" and expr.op == op:
+        out.append(expr.right)
+        expr = expr.left
+    out.append(expr)
+    return out[::-1]
+
+
+def _read_at(n, offset=None):
+    """(grid param, offset) of a Read node (optionally required at ``offset``), else None."""
+    if node_kind(n) != "Read":
+        return None
+    o = tuple(n.offset)
+    return None if offset is not None and o != tuple(offset) else (n.grid, o)
+
+
+def _const_times(n):
+    """(constant, other operand) of ``c * x`` or ``x * c``, else None."""
+    if node_kind(n) != "Binary" or n.op != "*":
+        return None
+    c = _const_value(n.left)
+    if c is not None:
+        return c, n.right
+    c = _const_value(n.right)
+    return (c, n.left) if c is not None else None
+
+
+def match_exact_wave(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
+    """XWAVE: the acoustic wave exactly as SURVEY.md §8(d) writes it (corpus.kernel_source
+    "wave"): ``A*u0 - p0 + k0 * (C0*u0 + L1*(S_1) + ... + LR*(S_R))`` with each S_m the six
+    axis taps in the order (-m,0,0), (m,0,0), (0,-m,0), (0,m,0), (0,0,-m), (0,0,m)."""
+    params = params if params is not None else dict(bmap.grid_args)
+    kern = bmap.kernel
+    if len(kern.updates) != 1 or kern.locals:
+        raise MatchError("not a single update without locals")
+    upd = kern.updates[0]
+    if len(upd.offset) != 3 or any(upd.offset):
+        raise MatchError("not a 3-D update at the centre")
+    e = upd.expr
+    zero = (0, 0, 0)
+    if node_kind(e) != "Binary" or e.op != "+":
+        raise MatchError("not head + kappa * laplacian")
+    head, tail = e.left, e.right
+    if node_kind(head) != "Binary" or head.op != "-":
+        raise MatchError("head is not A*u - p")
+    ct = _const_times(head.left)
+    p_rd = _read_at(head.right, zero)
+    if ct is None or p_rd is None or _read_at(ct[1], zero) is None:
+        raise MatchError("head is not A*u - p")
+    wave_a, u = ct[0], _read_at(ct[1], zero)[0]
+    p = p_rd[0]
+    if node_kind(tail) != "Binary" or tail.op != "*" or _read_at(tail.left, zero) is None:
+        raise MatchError("tail is not kappa * laplacian")
+    k = _read_at(tail.left, zero)[0]
+    terms = _chain(tail.right, "+")
+    first = _const_times(terms[0])
+    if first is None or _read_at(first[1], zero) != (u, zero):
+        raise MatchError("the laplacian does not start with C0 * u")
+    coef = [first[0]]
+    r = len(terms) - 1
+    if r < 1 or r > MAX_FAST_RADIUS:
+        raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
+    for m, t in enumerate(terms[1:], start=1):
+        ct = _const_times(t)
+        if ct is None:
+            raise MatchError("a ring term is not L_m * (sum)")
+        taps = _chain(ct[1], "+")
+        want = [(-m, 0, 0), (m, 0, 0), (0, -m, 0), (0, m, 0), (0, 0, -m), (0, 0, m)]
+        if len(taps) != 6 or [_read_at(x) for x in taps] != [(u, o) for o in want]:
+            raise MatchError(f"ring {m} is not the six axis taps of u in order")
+        coef.append(ct[0])
+    if len({u, p, k}) != 3:
+        raise MatchError("u, u_prev and kappa must be three grids")
+    src, dst, prev, vel = params[u], params[upd.dest], params[p], params[k]
+    if dst in (src, vel):
+        raise MatchError("wave update writes a grid it reads at a non-centre offset")
+    return MapPlan("xwave", r, src, dst, prev=prev, vel=vel, coef=coef, wave_a=wave_a, box=box)
 
 
 # ---------------------------------------------------------------------------

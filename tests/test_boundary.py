@@ -274,4 +274,46 @@ def test_exact_star_refuses_other_orders():
     short = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=e.left),))
     assert match_map(dataclasses.replace(m, kernel=short), exact=True).kind == "expr"
     wave, _ = corpus.config_target("wave", (8, 8, 8), 1)
-    assert match_map(next(_maps(wave.stmts)), exact=True).kind == "expr"
+    assert match_map(next(_maps(wave.stmts)), exact=True).kind == "xwave"
+
+
+def emulate_xwave(plan, state):
+    """CPU model of wave_exact_kernel's evaluation (star_exact.cuh): per ring m the six taps
+    d0-, d0+, d1-, d1+, d2-, d2+ summed left to right, the laplacian chain, then
+    (A*u - p) + k*lap, in float64 with one rounding."""
+    src, dst, prev, vel = state[plan.src], state[plan.dst], state[plan.prev], state[plan.vel]
+    R, o = plan.radius, src.order
+    box = plan.box
+    n = tuple(hi - lo for lo, hi in box)
+
+    def at(g, off):
+        d = g.data.astype(np.float64)
+        return d[tuple(slice(g.order + lo + q, g.order + lo + q + e) for (lo, _), q, e in zip(box, off, n))]
+
+    u0 = at(src, (0, 0, 0))
+    lap = plan.coef[0] * u0
+    for m in range(1, R + 1):
+        s = at(src, (-m, 0, 0)) + at(src, (m, 0, 0))
+        for off in ((0, -m, 0), (0, m, 0), (0, 0, -m), (0, 0, m)):
+            s = s + at(src, off)
+        lap = lap + plan.coef[m] * s
+    out = (plan.wave_a * u0 - at(prev, (0, 0, 0))) + at(vel, (0, 0, 0)) * lap
+    dst.data[tuple(slice(dst.order + lo, dst.order + hi) for lo, hi in box)] = out.astype(dst.data.dtype)
+
+
+@pytest.mark.parametrize("case", ["wave_16", "wave_f64_12"])
+def test_exact_wave_kernel_order_bitwise(case):
+    """precision='exact' routes the c3 acoustic wave to the exact wave kernel; its evaluation
+    order, modelled here, reproduces the reference's outputs bit for bit."""
+    meta, _, _, ins, outs = load_golden(case)
+    bound = build_case(meta)
+    state = {n: b.copy() for n, b in ins.items()}
+    for s in bound.stmts[0].body * bound.stmts[0].count:
+        if type(s).__name__ == "BoundSwap":
+            state[s.first], state[s.second] = state[s.second], state[s.first]
+        else:
+            plan = match_map(s, exact=True)
+            assert plan.kind == "xwave", plan.reason
+            emulate_xwave(plan, state)
+    for n, ref in outs.items():
+        assert np.array_equal(state[n].data, ref.data), n

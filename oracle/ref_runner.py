@@ -43,15 +43,20 @@ def load_manifest() -> dict:
     return json.loads(p.read_text())
 
 
-def library(entry: dict) -> tuple:
-    """Prefer a -march=native rebuild of the emitted C on this host."""
+def library(entry: dict, strict: bool = False) -> tuple:
+    """Prefer a -march=native rebuild of the emitted C on this host.  ``strict`` adds
+    -ffp-contract=off: no FMA contraction, so each product and sum rounds separately in
+    float64 as in run_target (the bit-exact comparison of precision='exact')."""
     src = REF / entry["source"]
+    flags = ["-O3", "-march=native", "-fopenmp"] + (["-ffp-contract=off"] if strict else [])
     if shutil.which("gcc") and src.exists():
-        out = Path(tempfile.gettempdir()) / f"stkb_ref_native_{os.getpid()}_{entry['lib']}"
-        r = subprocess.run(["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", str(src), "-o", str(out)],
-                           capture_output=True)
+        tag = "strict_" if strict else ""
+        out = Path(tempfile.gettempdir()) / f"stkb_ref_native_{tag}{os.getpid()}_{entry['lib']}"
+        r = subprocess.run(["gcc", *flags, "-fPIC", "-shared", str(src), "-o", str(out)], capture_output=True)
         if r.returncode == 0:
-            return out, "-O3 -march=native -fopenmp"
+            return out, " ".join(flags)
+    if strict:
+        raise RuntimeError("the strict (-ffp-contract=off) build of the reference C needs gcc on this host")
     return REF / entry["lib"], " ".join(entry["cflags"])
 
 
@@ -106,16 +111,17 @@ def run(name: str, steps: int, warmup: int) -> dict:
 _LOADED: dict = {}
 
 
-def call(name: str, arrays: list, steps: int) -> float:
+def call(name: str, arrays: list, steps: int, strict: bool = False) -> float:
     """Run the reference-emitted C of manifest entry ``name`` in this process on
     caller-owned padded arrays (in target-parameter order, mutated in place: the
     reference C-ABI, serial.py:126-208) for ``steps`` time steps; returns seconds.
     Test infrastructure: the parity tests' oracle at BASELINE sizes."""
     entry = load_manifest()[name]
-    if name not in _LOADED:
-        path, _ = library(entry)
-        _LOADED[name] = ctypes.CDLL(str(path))
-    fn = getattr(_LOADED[name], entry["entry"])
+    key = (name, strict)
+    if key not in _LOADED:
+        path, _ = library(entry, strict)
+        _LOADED[key] = ctypes.CDLL(str(path))
+    fn = getattr(_LOADED[key], entry["entry"])
     cty = ctypes.c_float if entry["dtype"] == "f32" else ctypes.c_double
     dt = np.float32 if entry["dtype"] == "f32" else np.float64
     order = _order(entry["builder"])

@@ -216,3 +216,60 @@ def test_c5_full_grid_n_steps_vs_reference_cpu_windows(case, builder, radius, re
             assert scale > 0 and max_rel <= TOL[dtype], (case, z0, n, max_rel)
         result["windows"][str(z0)] = rec
     _record(case, **result)
+
+
+EXACT = [
+    ("c4", "star3d4r_norm", (1024, 1024, 1024), "f32", 10, "p_c4_star3d4r_norm"),
+    ("c3", "wave", (1024, 1024, 1024), "f32", 3, None),
+    ("c2", "jacobi7", (512, 512, 512), "f32", 20, "p_c2_jacobi7"),
+]
+
+
+@pytest.mark.parametrize("case,builder,shape,dtype,steps,ref_name", EXACT, ids=[c[0] for c in EXACT])
+def test_full_size_exact_path_bitwise_vs_reference_cpu(case, builder, shape, dtype, steps, ref_name):
+    """precision='exact' at the BASELINE sizes (the exact streaming kernels), bit for bit.
+
+    Stars: against the reference-emitted C built without FMA contraction (every term is
+    ``double * float`` and every sum is in float64, as in run_target).  The wave: against the
+    pinned C restatement of run_target (oracle/stkoracle.c) — the reference's own emitted C is
+    NOT bit-identical to its oracle there: ``u[a] + u[b]`` of two ``float`` taps is a
+    single-precision addition in C, while run_target sums in float64 (executor.py:1-10)."""
+    bound, decls = corpus.config_target(builder, shape, steps, dtype)
+    names = [g for _, g in bound.grid_params]
+    body = next(s for s in bound.stmts if type(s).__name__ == "BoundFor").body
+    GridBuffer = front.module("grids").GridBuffer
+    dummies = {n: GridBuffer(decls[n].dtype, tuple(decls[n].shape), decls[n].order, np.zeros((1, 1, 1)))
+               for n in names}
+    with DeviceTarget(dummies, names, precision="exact") as dt:
+        if builder == "wave":
+            _fill_wave(dt)
+        else:
+            for n in names:
+                _interior(dt, n).zero_()
+            _fill_loguniform(_interior(dt, names[0]), 9)
+        _torch().cuda.synchronize()
+        host = {n: dt.download(n) for n in names}
+        dt.set_program(body)
+        dt.run(steps)
+        dt.sync()
+        kinds = sorted({p.kind for p in dt.plans})
+        got = {n: dt.download(n) for n in names}
+    assert kinds in (["xstar"], ["xwave"]), kinds
+    if ref_name is None:
+        from oracle import oracle
+
+        order = decls[names[0]].order
+        ins = {n: GridBuffer(dtype, shape, order, host[n]) for n in names}
+        outs = oracle.run_target_c(bound, ins)
+        host = {n: outs[n].data for n in names}
+        what = "oracle/stkoracle.c (run_target's float64 evaluation, pinned to the reference goldens)"
+    else:
+        ref_runner.call(ref_name, [host[n] for n in names], steps, strict=True)
+        what = f"oracle/_ref/{ref_name}.c built with -ffp-contract=off"
+    result = {"shape": list(shape), "dtype": dtype, "steps": steps, "device_kernel": kinds[0],
+              "oracle": what, "bitwise_equal": {}}
+    for n in names:
+        same = bool(np.array_equal(host[n].view(np.uint32), got[n].view(np.uint32)))
+        result["bitwise_equal"][n] = same
+        assert same, (case, n, float(np.abs(host[n].astype(np.float64) - got[n]).max()))
+    _record(f"{case}_exact", **result)

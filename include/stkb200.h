@@ -195,6 +195,10 @@ int stkb_launch_map(stkb_domain *dom, int32_t map_index, int64_t lo0, int64_t hi
 int stkb_launch_map_ranges(stkb_domain *dom, int32_t map_index, int32_t n_ranges, const int64_t *lo0,
                            const int64_t *hi0, int32_t n_signal, int32_t *signal_items);
 int stkb_stream_wait_signal(stkb_domain *dom, void *stream, int32_t map_index, int32_t value);
+/* Zero map `map_index`'s signal counter on `stream` (NULL = the domain's): a caller that resets
+ * it before every launch waits for that launch's own signal_items, so the same wait value
+ * repeats every step and the step can be captured into a CUDA graph and replayed. */
+int stkb_reset_signal(stkb_domain *dom, int32_t map_index, void *stream);
 int stkb_set_max_ctas(stkb_domain *dom, int32_t ctas); /* 0 = one CTA per SM (leave SMs for NCCL) */
 
 /* Two time steps per d0 sweep (temporal blocking, on by default): when the step

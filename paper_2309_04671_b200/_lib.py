@@ -34,7 +34,7 @@ EXPORTS = (
     "stkb_program_add_map", "stkb_program_add_swap", "stkb_run", "stkb_run_once", "stkb_sync",
     "stkb_elapsed_ms", "stkb_launches", "stkb_run_mode", "stkb_binding", "stkb_nonfinite", "stkb_run_target",
     "stkb_compare", "stkb_launch_map", "stkb_apply_swap", "stkb_plane_span", "stkb_launch_map_ranges",
-    "stkb_stream_wait_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
+    "stkb_stream_wait_signal", "stkb_reset_signal", "stkb_set_max_ctas", "stkb_launch_map_pull", "stkb_peer_fetch_halo", "stkb_buffer_ipc_handle",
     "stkb_flags_ipc_handle", "stkb_buffer_ptr", "stkb_flags_ptr", "stkb_ipc_open", "stkb_ipc_close", "stkb_set_peer",
     "stkb_peer_signal", "stkb_peer_wait", "stkb_set_fused_steps", "stkb_set_multi_steps", "stkb_enable_peer", "stkb_prepare",
 )
@@ -136,6 +136,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "stkb_plane_span": [V, i32, i64, i64, P(V), P(i64)],
         "stkb_launch_map_ranges": [V, i32, i32, P(i64), P(i64), i32, P(i32)],
         "stkb_stream_wait_signal": [V, V, i32, i32],
+        "stkb_reset_signal": [V, i32, V],
         "stkb_set_max_ctas": [V, i32],
         "stkb_set_fused_steps": [V, i32],
         "stkb_set_multi_steps": [V, i32, i64],

@@ -1586,6 +1586,15 @@ int stkb_stream_wait_signal(stkb_domain* dom, void* stream, int32_t map_index, i
     return STKB_OK;
 }
 
+int stkb_reset_signal(stkb_domain* dom, int32_t map_index, void* stream) {
+    if (!dom) return fail(STKB_ERR_ARG, "null domain");
+    if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
+    CUDA_TRY(cudaSetDevice(dom->desc.device));
+    int32_t* sig = dom->d_flags + kMaxTags + kMaxMaps + dom->maps[map_index].slot;
+    CUDA_TRY(cudaMemsetAsync(sig, 0, sizeof(int32_t), stream ? static_cast<cudaStream_t>(stream) : dom->stream));
+    return STKB_OK;
+}
+
 int stkb_prepare(stkb_domain* dom) {
     if (!dom) return fail(STKB_ERR_ARG, "null domain");
     CUDA_TRY(cudaSetDevice(dom->desc.device));

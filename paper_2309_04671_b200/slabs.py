@@ -291,7 +291,6 @@ class DeviceSlabEngine:
         self.dt.set_stream(self.compute.cuda_stream)
         self.tdtype = torch.float32 if d0.dtype == "f32" else torch.float64
         self.launches = 0
-        self.signal_target = {}  # map index -> running sum of its boundary signal
         self.t = 0  # exchanged launches issued (p2p flags)
         self.graphs = {}  # (binding, t mod 3) -> (CUDA graph of graph_period() steps, launches, kernels)
         self._dist = None
@@ -362,7 +361,11 @@ class DeviceSlabEngine:
         L.call("stkb_apply_swap", self.dt.h, self.dt.index[a], self.dt.index[b])
 
     def launch_with_boundary(self, i: int, r: int):
-        """One launch: boundary items first (each bumps the map's signal), then the interior."""
+        """One launch: boundary items first (each bumps the map's signal), then the interior.
+
+        The signal counter is zeroed on the compute stream right before the launch and the
+        exchange stream forks from there (event), so it waits for exactly this launch's
+        boundary items: the wait value repeats every step (graph-capturable)."""
         from . import _lib as L
 
         rng = boundary_ranges(self.plan.size, r)
@@ -371,16 +374,20 @@ class DeviceSlabEngine:
         nsig = min(2, len(rng)) if len(rng) > 1 else 1
         items = ctypes.c_int32()
         k = self.map_index[i]
+        L.call("stkb_reset_signal", self.dt.h, k, ctypes.c_void_p(self.compute.cuda_stream))
+        fork = self.torch.cuda.Event()
+        fork.record(self.compute)
         L.call("stkb_launch_map_ranges", self.dt.h, k, len(rng), lo, hi, nsig, ctypes.byref(items))
         self.launches += 1
-        self.signal_target[k] = self.signal_target.get(k, 0) + items.value
-        return k, self.signal_target[k]
+        return k, items.value, fork
 
     def comm_context(self, token):
         from . import _lib as L
 
-        k, target = token
-        # the exchange stream waits (no SM held) until every boundary item is stored
+        k, target, fork = token
+        # the exchange stream joins after the counter reset, then waits (no SM held) until
+        # every boundary item of the launch is stored
+        self.comm.wait_event(fork)
         L.call("stkb_stream_wait_signal", self.dt.h, ctypes.c_void_p(self.comm.cuda_stream), k,
                ctypes.c_int32(target & 0x7FFFFFFF))
         return self.torch.cuda.stream(self.comm)
@@ -424,12 +431,69 @@ class DeviceSlabEngine:
         flag = 3 // math.gcd(maps, 3) if maps else 1
         return bp * flag // math.gcd(bp, flag)
 
+    def binding_period(self) -> int:
+        names = list(self.dt.names)
+        bind = {n: n for n in names}
+        start = dict(bind)
+        bp = 0
+        while True:
+            for s in self.body:
+                if stmt_kind(s) == "BoundSwap":
+                    bind[s.first], bind[s.second] = bind[s.second], bind[s.first]
+            bp += 1
+            if bind == start:
+                return bp
+
+    def _run_nccl_graphs(self, n: int, dist) -> int:
+        """NCCL transport as CUDA graphs of one binding period (kernels, counter resets,
+        stream waits and the NCCL send/recv on the exchange stream), after one eager step
+        has initialised the communicators.  Opt-in (STKB_NCCL_GRAPHS=1): it has not been run
+        across two physical GPUs.  Returns the steps left to run eagerly."""
+        torch = self.torch
+        if not getattr(self, "_nccl_warm", False):
+            return n
+        period = self.binding_period()
+        while n >= period:
+            key = ("nccl", self.binding())
+            hit = self.graphs.get(key)
+            if hit is None:
+                from . import _lib as L
+
+                L.call("stkb_prepare", self.dt.h)
+                g = torch.cuda.CUDAGraph()
+                l0 = self.launches
+                saved = self.binding()
+                with torch.cuda.stream(self.compute):
+                    g.capture_begin(capture_error_mode="thread_local")
+                    try:
+                        for _ in range(period):
+                            run_step(self, dist)  # swaps advance the host binding as if run
+                    finally:
+                        g.capture_end()
+                hit = self.graphs[key] = (g, self.launches - l0)
+                self.launches = l0
+                assert self.binding() == saved  # one binding period: back where it started
+            g, dl = hit
+            with torch.cuda.stream(self.compute):
+                g.replay()
+            self.launches += dl
+            n -= period
+        return n
+
     def run(self, n: int, dist=None) -> None:
         """n time steps.  With the fused exchange the steps replay as CUDA graphs of
         `graph_period()` steps (kernels and stream memory operations captured once per
-        starting binding), the remainder directly."""
+        starting binding), the remainder directly; the NCCL transport replays graphs of one
+        binding period when STKB_NCCL_GRAPHS=1."""
         import os
 
+        if (self.transport == "nccl" and self.plan.world > 1 and dist is not None
+                and os.environ.get("STKB_NCCL_GRAPHS") == "1"):
+            if not getattr(self, "_nccl_warm", False) and n > 0:
+                self.step(dist)
+                self._nccl_warm = True
+                n -= 1
+            n = self._run_nccl_graphs(n, dist)
         use = (self.transport == "p2p" and self.plan.world > 1 and self.peers_connected
                and os.environ.get("STKB_SLAB_GRAPHS", "1") != "0")
         if use:

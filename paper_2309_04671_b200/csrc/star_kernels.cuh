@@ -32,9 +32,11 @@ namespace stkb {
 
 enum { FORM_STAR = 0, FORM_STAR_DIV = 1, FORM_WAVE = 2, FORM_BOX = 3, FORM_BOX_DIV = 4 };
 
-template <typename T, int R, int FORM, int TY, int NWY>
+template <typename T, int R, int FORM, int TY, int NWY, int LW = 0>
 struct StarCfg {
-    static constexpr int VEC = 16 / sizeof(T);
+    // elements per lane: one 16-byte vector by default, LW (a multiple of it) when given
+    static constexpr int VEC = LW > 0 ? LW : int(16 / sizeof(T));
+    static_assert((VEC * sizeof(T)) % 16 == 0, "a lane holds whole 16-byte vectors");
     static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;  // x-halo rounded to a vector
     static constexpr int BX = 32 * VEC;
     static constexpr int BY = NWY * TY;
@@ -74,6 +76,26 @@ __device__ __forceinline__ void lds16(const float* p, float* v) {
 }
 __device__ __forceinline__ void lds16(const double* p, double* v) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(smem_u32(p)));
+}
+
+// N consecutive elements (whole 16-byte vectors): shared loads / global stores
+template <typename T, int N>
+__device__ __forceinline__ void ldsv(const T* p, T* v) {
+    constexpr int E = 16 / sizeof(T);
+#pragma unroll
+    for (int k = 0; k < N / E; ++k) lds16(p + k * E, v + k * E);
+}
+template <typename T, int N>
+__device__ __forceinline__ void stgv(T* p, const T (&v)[N], bool streaming) {
+    constexpr int E = 16 / sizeof(T);
+#pragma unroll
+    for (int k = 0; k < N / E; ++k) {
+        T w[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) w[i] = v[k * E + i];
+        if (streaming) stg16_cs(p + k * E, w);
+        else stg16(p + k * E, w);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -171,7 +193,18 @@ __device__ __noinline__ void store_row_masked(T* dz, T v0, T v1, T v2, T v3, int
         if (x + i >= lo2 && x + i < hi2) dz[i] = v[i];
 }
 
-template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL>
+// the same for N <= 4 values per lane, passed by value (an array argument would push the
+// caller's output row through local memory on every plane)
+template <typename T, int N>
+__device__ __noinline__ void store_row_masked_n(T* dz, T v0, T v1, T v2, T v3, int x, int lo2, int hi2) {
+    static_assert(N <= 4, "at most 4 values per lane");
+    const T v[4] = {v0, v1, v2, v3};
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (x + i >= lo2 && x + i < hi2) dz[i] = v[i];
+}
+
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL, int LW = 0>
 __global__ void __launch_bounds__((NWY + 1) * 32, 1)
 star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_ctr,
@@ -181,7 +214,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_hi,   // upper neighbour's src (a.pull & 2)
                    const __grid_constant__ CUtensorMap tm_int,  // src interior only (a.halo_nz)
                    const __grid_constant__ StarArgs<T> a) {
-    using C = StarCfg<T, R, FORM, TY, NWY>;
+    using C = StarCfg<T, R, FORM, TY, NWY, LW>;
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW;
     constexpr int STAGES = C::STAGES;
     constexpr int NS = 2 * R + 1;
@@ -392,10 +425,10 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                             const T* row = t + (jr0 + rr) * SW + xl;
 #pragma unroll
                             for (int k = 0; k < RA / VEC; ++k) {
-                                lds16(row + k * VEC, &xr[k * VEC]);
-                                lds16(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
+                                ldsv<T, VEC>(row + k * VEC, &xr[k * VEC]);
+                                ldsv<T, VEC>(row + RA + VEC + k * VEC, &xr[RA + VEC + k * VEC]);
                             }
-                            lds16(row + RA, &xr[RA]);
+                            ldsv<T, VEC>(row + RA, &xr[RA]);
 #pragma unroll
                             for (int j = 0; j < TY; ++j) {
                                 const int dy = rr - (j + R);
@@ -432,7 +465,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                         // centre values of this thread's rows in plane q
                         T cvs[TY][VEC];
     #pragma unroll
-                        for (int j = 0; j < TY; ++j) lds16(t + (jr0 + j + R) * SW + xl + RA, cvs[j]);
+                        for (int j = 0; j < TY; ++j) ldsv<T, VEC>(t + (jr0 + j + R) * SW + xl + RA, cvs[j]);
                         P cv[TY][NPK];
     #pragma unroll
                         for (int j = 0; j < TY; ++j)
@@ -449,8 +482,8 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                 const T* row = t + (jr0 + j + R) * SW + xl;
     #pragma unroll
                                 for (int k = 0; k < RA / VEC; ++k) {
-                                    lds16(row + k * VEC, &xr[j][k * VEC]);
-                                    lds16(row + RA + VEC + k * VEC, &xr[j][RA + VEC + k * VEC]);
+                                    ldsv<T, VEC>(row + k * VEC, &xr[j][k * VEC]);
+                                    ldsv<T, VEC>(row + RA + VEC + k * VEC, &xr[j][RA + VEC + k * VEC]);
                                 }
     #pragma unroll
                                 for (int i = 0; i < VEC; ++i) xr[j][RA + i] = cvs[j][i];
@@ -498,7 +531,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                     }
                                 } else {
                                     T yv[VEC];
-                                    lds16(t + (jr0 + rr) * SW + xl + RA, yv);
+                                    ldsv<T, VEC>(t + (jr0 + rr) * SW + xl + RA, yv);
     #pragma unroll
                                     for (int j = 0; j < TY; ++j) {
                                         const int m = rr - (j + R);
@@ -566,20 +599,16 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     if (z_out) {
                         T* const dz = dst0 + (int64_t(z) + a.g.order0) * plane;
                         if (full_tile) {
-                            if (a.store_hint) {
 #pragma unroll
-                                for (int j = 0; j < TY; ++j) stg16_cs(dz + j * pitch, outv[j]);
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < TY; ++j) stg16(dz + j * pitch, outv[j]);
-                            }
+                            for (int j = 0; j < TY; ++j) stgv<T, VEC>(dz + j * pitch, outv[j], a.store_hint != 0);
                         } else if (x_any) {
 #pragma unroll
                             for (int j = 0; j < TY; ++j) {
                                 const int y = y0 + jr0 + j;
                                 if (y >= a.box.lo1 && y < a.box.hi1)
-                                    store_row_masked<T>(dz + j * pitch, outv[j][0], outv[j][1 % VEC],
-                                                        outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2, a.box.hi2);
+                                    store_row_masked_n<T, VEC>(dz + j * pitch, outv[j][0], outv[j][1 % VEC],
+                                                               outv[j][2 % VEC], outv[j][3 % VEC], x, a.box.lo2,
+                                                               a.box.hi2);
                             }
                         }
                     }
@@ -662,10 +691,10 @@ inline int chunk_range(int lo, int n0, int lz, int tiles, int ctas, bool taper, 
     return k;
 }
 
-template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL>
+template <typename T, int R, int FORM, int TY, int NWY, bool ODD_SCALAR, bool PULL, int LW = 0>
 cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMap* maps, cudaStream_t stream) {
-    using C = StarCfg<T, R, FORM, TY, NWY>;
-    auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR, PULL>;
+    using C = StarCfg<T, R, FORM, TY, NWY, LW>;
+    auto kern = star_stream_kernel<T, R, FORM, TY, NWY, ODD_SCALAR, PULL, LW>;
     // a tensor-map box that differs from this instantiation's tile would make the
     // mbarrier transaction counts disagree (a hang): refuse instead
     if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
@@ -756,8 +785,9 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
     return cudaGetLastError();
 }
 
-// tile variants: (rows per warp, consumer warps, odd x-taps as scalar FMAs)
-struct Variant { int ty, nwy; bool odd_scalar; };
+// tile variants: (rows per warp, consumer warps, odd x-taps as scalar FMAs, elements per lane
+// (0: one 16-byte vector))
+struct Variant { int ty, nwy; bool odd_scalar; int lw = 0; };
 
 template <typename T>
 __host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = false) {
@@ -771,6 +801,11 @@ __host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = f
         case 6: return Variant{2, 9, true};
         case 7: return Variant{2, 12, true};
         case 8: return Variant{3, 8, true};
+        // 32-byte lanes (fp64: 4 values per lane, 128-wide tiles): the ring of 2 rows x 4 values
+        // needs ~190 registers, i.e. at most 2 warps per SM sub-partition (8 warps per CTA)
+        case 10: return sizeof(T) == 8 ? Variant{2, 7, true, 4} : Variant{2, 11, true};
+        case 11: return sizeof(T) == 8 ? Variant{2, 6, true, 4} : Variant{2, 11, true};
+        case 12: return sizeof(T) == 8 ? Variant{1, 11, true, 4} : Variant{2, 11, true};
         default:  // measured best on B200 per form, dtype and radius (tools/sweep.py)
             // dense cubes: R=1 4 rows/warp (rows share taps), R=2 one row, R=3..4 one row with
             // 11 warps (up to 170 registers); R=4 forms odd-shift pairs once per row (+13 %)
@@ -802,9 +837,10 @@ cudaError_t launch_star_vp(const StarLaunch& L, const StarArgs<T>& a, const CUte
             return launch_star_cfg<T, R, FORM_BOX, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
         }
     }
-    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
-    if (L.has_divisor) return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
-    return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar, PULL>(L, a, maps, s);
+    if (L.kind == 2) return launch_star_cfg<T, R, FORM_WAVE, vv.ty, vv.nwy, vv.odd_scalar, PULL, vv.lw>(L, a, maps, s);
+    if (L.has_divisor)
+        return launch_star_cfg<T, R, FORM_STAR_DIV, vv.ty, vv.nwy, vv.odd_scalar, PULL, vv.lw>(L, a, maps, s);
+    return launch_star_cfg<T, R, FORM_STAR, vv.ty, vv.nwy, vv.odd_scalar, PULL, vv.lw>(L, a, maps, s);
 }
 
 // the neighbour-reading (multi-GPU) kernels are separate instantiations: the
@@ -834,6 +870,9 @@ cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUten
             case 6: return launch_star_v<T, R, 6>(L, a, maps, s);
             case 7: return launch_star_v<T, R, 7>(L, a, maps, s);
             case 8: return launch_star_v<T, R, 8>(L, a, maps, s);
+            case 10: return launch_star_v<T, R, 10>(L, a, maps, s);
+            case 11: return launch_star_v<T, R, 11>(L, a, maps, s);
+            case 12: return launch_star_v<T, R, 12>(L, a, maps, s);
             default: break;
         }
     }
@@ -854,9 +893,9 @@ cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUten
 // tile geometry used to build the tensor-map boxes on the host
 template <typename T>
 inline void star_tile_t(int R, bool box, int* bx, int* by, int* halo_x) {
-    constexpr int VEC = 16 / sizeof(T);
     const int v = STKB_VARIANTS > 1 ? star_variant_env() : 0;
     const Variant vv = star_variant_of<T>(R, v, box);
+    const int VEC = vv.lw > 0 && !box ? vv.lw : int(16 / sizeof(T));
     *bx = 32 * VEC;
     *by = vv.nwy * vv.ty;
     *halo_x = ((R + VEC - 1) / VEC) * VEC;

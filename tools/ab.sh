@@ -5,6 +5,6 @@ A=$1; B=$2; shift 2
 for r in 1 2; do
   for L in $A $B; do
     echo "== $(basename $L) round $r"
-    STKB_LIB=$L python tools/sweep.py "$@" 2>&1 | grep gpts
+    STKB_LIB_LENIENT=1 STKB_LIB=$L python tools/sweep.py "$@" 2>&1 | grep gpts
   done
 done

@@ -19,7 +19,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 WATCH = ("UTMALDG", "SYNCS", "FFMA2", "FFMA", "DFMA", "FMUL2", "LDS.128", "LDS", "STG.E.128", "STG", "LDG",
-         "SHFL", "LDCU", "BAR", "ATOMG", "RED")
+         "SHFL", "LDCU", "BAR", "ATOMG", "RED", "STL", "LDL")  # STL/LDL: local memory (spills, stack arrays)
 
 
 def demangle(names):

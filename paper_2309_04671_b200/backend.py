@@ -164,7 +164,8 @@ class DeviceTarget:
         ext = (ctypes.c_int64 * 3)(*shape)
         L.call("stkb_upload_grid", self.h, self.index[name], arr.ctypes.data_as(ctypes.c_void_p), ext, order,
                int(bool(sync)))
-        self._keep = arr
+        if not sync:  # the host array must outlive the asynchronous copy: kept until sync()
+            self._pending = getattr(self, "_pending", []) + [arr]
 
     def download(self, name: str, out: Optional[np.ndarray] = None, sync: bool = True) -> np.ndarray:
         shape, order = self.buffer_layout(name)
@@ -246,6 +247,7 @@ class DeviceTarget:
 
     def sync(self) -> None:
         L.call("stkb_sync", self.h)
+        self._pending = []
 
     def elapsed_ms(self) -> float:
         v = ctypes.c_double()

@@ -168,6 +168,7 @@ struct stkb_domain {
     int64_t halo_epoch = 0;
     // several ping-pong steps per launch for small grids (star_kernels.cuh, StarArgs::n_steps)
     int32_t* d_multi = nullptr;    // per-step work counters + the step-arrive counter
+    cudaError_t last_launch_error = cudaSuccess;
     int64_t multi_max_points = int64_t(1) << 25;  // STKB_MULTI_POINTS: grids up to this many points
     bool multi = true;             // STKB_MULTI=0 disables
     bool halo_external = false;  // z-slab machinery writes halo planes (exchange, peers): full maps only
@@ -491,6 +492,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     } else {
         e = launch_star_f64(L, a, dom->stream);
     }
+    dom->last_launch_error = e;
     if (e != cudaSuccess) return fail(STKB_ERR_CUDA, std::string("star kernel launch: ") + cudaGetErrorString(e));
     return STKB_OK;
 }
@@ -1155,6 +1157,12 @@ int stkb_run(stkb_domain* dom, int64_t steps) {
             const int rc = dom->desc.dtype == STKB_F32
                                ? launch_star_map<float>(dom, *mm, dom->binding, RangeSpec(), false, n)
                                : launch_star_map<double>(dom, *mm, dom->binding, RangeSpec(), false, n);
+            if (rc && done == 0 && dom->last_launch_error == cudaErrorCooperativeLaunchTooLarge) {
+                cudaGetLastError();  // not sticky: clear it
+                // not every CTA could be resident (the device is shared): single steps instead
+                dom->multi = false;
+                return stkb_run(dom, steps);
+            }
             if (rc) return rc;
             ++launches;
             if (n & 1) std::swap(dom->binding[mm->d.src], dom->binding[mm->d.dst]);

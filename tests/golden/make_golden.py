@@ -7,9 +7,8 @@ Run in the build container (where /root/reference exists):
 For every case it writes tests/golden/<case>.npz holding
   * ``source``: the .stpy program text, parsed by the reference front end
     (parser.parse_source + validate) and bound by analysis.bind_target;
-  * ``dump``: the canonical dump of the reference's BoundTarget
-    (paper_2309_04671_b200.program.dump), which the tests compare with the
-    program this package builds for the same case;
+  * ``dump``: the reference's own analysis dump of the bound program
+    (stencilkit.analysis.dump_analysis), for inspection;
   * ``in_<grid>`` / ``out_<grid>``: padded inputs (reference
     grids.fill_loguniform, or the c3 wave initialiser) and the reference
     executor.run_target outputs (float64 accumulate, one rounding).
@@ -31,13 +30,12 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(REF))
 
 from stencilkit import corpus as ref_corpus  # noqa: E402
-from stencilkit.analysis import bind_target  # noqa: E402
+from stencilkit.analysis import bind_target, dump_analysis  # noqa: E402
 from stencilkit.executor import run_target  # noqa: E402
 from stencilkit.grids import GridBuffer, fill_loguniform  # noqa: E402
 from stencilkit.parser import parse_source, validate  # noqa: E402
 
 from paper_2309_04671_b200 import corpus  # noqa: E402
-from paper_2309_04671_b200.program import dump  # noqa: E402
 
 # (case, builder, shape, iters, dtype, map_width, scheme, seed)
 CASES = [
@@ -59,18 +57,9 @@ CASES = [
 
 
 def source_for(builder, shape, iters, dtype, width):
-    if builder == "wave":
-        return corpus.source_text(corpus.wave_kernel(), shape, 4, iters, dtype, swap=("up", "u"),
-                                  map_width=width, target="target_acoustic_iso")
-    if builder == "jacobi7":
-        return corpus.source_text(corpus.jacobi7_kernel(), shape, 1, iters, dtype, map_width=width,
-                                  target="target_jacobi7")
-    if builder.endswith("_norm"):
-        base = builder.removesuffix("_norm")
-        return corpus.source_text(corpus.normalised_star_kernel(base), shape, corpus.KERNELS[base].radius,
-                                  iters, dtype, map_width=width, target=f"target_{builder}")
-    # the corpus kernels: the reference's own source_text
-    return ref_corpus.source_text(builder, shape=shape, iters=iters, dtype=dtype, map_width=width)
+    if builder in corpus.KERNELS:  # the corpus kernels: the reference's own source_text
+        return ref_corpus.source_text(builder, shape=shape, iters=iters, dtype=dtype, map_width=width)
+    return corpus.program_text(builder, shape, iters, dtype, width)
 
 
 def main() -> None:
@@ -93,7 +82,8 @@ def main() -> None:
         meta = dict(case=case, builder=builder, shape=list(shape), iters=iters, dtype=dtype, map_width=width,
                     scheme=scheme or "cross_product", seed=seed, numpy=np.__version__,
                     reference=f"stencilkit {stencilkit.__version__}")
-        np.savez_compressed(HERE / f"{case}.npz", meta=json.dumps(meta), source=text, dump=dump(bound), **arrays)
+        np.savez_compressed(HERE / f"{case}.npz", meta=json.dumps(meta), source=text, dump=dump_analysis(unit, bound),
+                            **arrays)
         print(case, "ok")
 
 

@@ -24,6 +24,10 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT
          f"-DSTKB_VARIANTS={int(os.environ.get('STKB_BUILD_VARIANTS', '1'))}"]
 if os.environ.get("STKB_BUILD_MAX_STAGES"):  # experiments: deeper TMA rings
     FLAGS.append(f"-DSTKB_MAX_STAGES={int(os.environ['STKB_BUILD_MAX_STAGES'])}")
+if os.environ.get("STKB_BUILD_EXP_L2SRC"):  # experiment: L2-resident source planes
+    FLAGS.append(f"-DSTKB_EXP_L2SRC={int(os.environ['STKB_BUILD_EXP_L2SRC'])}")
+if os.environ.get("STKB_BUILD_MBAR_SUSPEND_NS"):  # experiments: suspending mbarrier waits
+    FLAGS.append(f"-DSTKB_MBAR_SUSPEND_NS={int(os.environ['STKB_BUILD_MBAR_SUSPEND_NS'])}")
 
 
 def nvcc() -> str:

@@ -136,7 +136,21 @@ __device__ __forceinline__ void mbar_arrive_lane0(uint64_t* bar, int lane) {
                  ::"r"(smem_u32(bar)), "r"(lane) : "memory");
 }
 
+// STKB_MBAR_SUSPEND_NS > 0: each try_wait may suspend the warp up to that long (woken when the
+// phase completes) instead of returning at once and spinning (experiment switch)
+#ifndef STKB_MBAR_SUSPEND_NS
+#define STKB_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if STKB_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(smem_u32(bar)), "r"(parity), "r"(uint32_t(STKB_MBAR_SUSPEND_NS)) : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
@@ -144,6 +158,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t"
         "}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+#endif
 }
 
 // 3-D tiled TMA load global -> shared, completion counted on `bar`.

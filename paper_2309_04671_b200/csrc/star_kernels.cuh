@@ -183,6 +183,11 @@ __device__ __forceinline__ void decode_item(const A& a, int item, int& tx, int& 
     }
 }
 
+// streaming (evict-first) output stores: a compile-time experiment switch (measured ±1 %)
+#ifndef STKB_STORE_STREAMING
+#define STKB_STORE_STREAMING false
+#endif
+
 // cold path: one output row of a tile that straddles the region box
 template <typename T>
 __device__ __noinline__ void store_row_masked(T* dz, T v0, T v1, T v2, T v3, int x, int lo2, int hi2) {
@@ -303,7 +308,13 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                         T* st = tiles + size_t(s) * C::STAGE_ELEMS;
                         // src plane q: this slab's own (incl. its halo), or a neighbour's over NVLink
                         const CUtensorMap* hm = own;
+#ifdef STKB_EXP_L2SRC
+                        // experiment: every plane read from a window of STKB_EXP_L2SRC planes (an
+                        // L2-resident source: the kernel's rate with HBM writes only)
+                        int hz = ((q % STKB_EXP_L2SRC) + STKB_EXP_L2SRC) % STKB_EXP_L2SRC + int(a.g.order0) - iz;
+#else
                         int hz = q + int(a.g.order0) - iz;
+#endif
                         int hx = c0 - ix, hy = c1 - iy;
                         if constexpr (PULL) {
                             if (q < 0 && (a.pull & 1)) {
@@ -397,8 +408,10 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
         const bool full_tile = x0 >= a.box.lo2 && x0 + BX <= a.box.hi2 && y0 >= a.box.lo1 && y0 + BY <= a.box.hi1;
         const bool x_full = (x >= a.box.lo2) && (x + VEC <= a.box.hi2);
         const bool x_any = (x + VEC > a.box.lo2) && (x < a.box.hi2);
-        // output address of row jr0 at plane z: dst0 + (z + order0) * plane + j * pitch
-        T* const dst0 = dst_step + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x;
+        // output address of row jr0 at plane z = q - R: advanced by one plane per stage (no
+        // 64-bit multiply per plane); starts at plane z0 - 2R for q = z0 - R
+        T* dzp = dst_step + (int64_t(y0 + jr0) + a.g.order) * pitch + a.g.lead + x +
+                 (int64_t(z0) - 2 * R + a.g.order0) * plane;
 
         // the plane loop is unrolled by 2R+1 so the accumulator ring slots are static
         // registers; the wide dense boxes (R > 2: 343 / 729 taps per plane) keep one plane
@@ -597,10 +610,10 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                     ++it;
 
                     if (z_out) {
-                        T* const dz = dst0 + (int64_t(z) + a.g.order0) * plane;
+                        T* const dz = dzp;
                         if (full_tile) {
 #pragma unroll
-                            for (int j = 0; j < TY; ++j) stgv<T, VEC>(dz + j * pitch, outv[j], a.store_hint != 0);
+                            for (int j = 0; j < TY; ++j) stgv<T, VEC>(dz + j * pitch, outv[j], STKB_STORE_STREAMING);
                         } else if (x_any) {
 #pragma unroll
                             for (int j = 0; j < TY; ++j) {
@@ -612,6 +625,7 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                             }
                         }
                     }
+                    dzp += plane;
                     if constexpr (ROT) {
                         // output o lives in slot (o - q) mod NS: move every slot down by one
 #pragma unroll

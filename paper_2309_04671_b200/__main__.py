@@ -1,7 +1,7 @@
 """``python -m paper_2309_04671_b200 <command> ...`` — the reference CLI on B200.
 
 Runs the reference's own command line (``stencilkit.cli.main``: ``run``,
-``check``, ``analyze``, ``diff``, ...) with the drop-in installed
+``compile``, ``inspect``, ``simulate``, ``diff``) with the drop-in installed
 (:func:`.integrate.install`), so ``run --backend gpu`` (cli.py:246-283)
 executes the bound target on the device: same flags, same STG1 output
 files, same ``--oracle`` report and exit codes (0 ok, 1 diagnostics, 2

@@ -273,7 +273,7 @@ cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaS
 cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
 cudaError_t launch_exact_f32(const StarLaunch& L, const StarArgs<float>& a, const XstarCoef& xc, cudaStream_t s);
 cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, const XstarCoef& xc, cudaStream_t s);
-int exact_tile(int dtype, int radius, int* bx, int* by, int* halo_x);
+int exact_tile(int dtype, int radius, bool wave, int* bx, int* by, int* halo_x);
 cudaError_t launch_xwave_f32(const StarLaunch& L, const StarArgs<float>& a, const XwaveCoef& xc, cudaStream_t s);
 cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, const XwaveCoef& xc, cudaStream_t s);
 }  // namespace stkb

@@ -19,18 +19,32 @@ cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, con
     return launch_xwave_t<double>(L, a, xc, L.maps, s);
 }
 
-// exact star and exact wave share the tile shape (one output row per warp, 15 warps)
-int exact_tile(int dtype, int radius, int* bx, int* by, int* halo_x) {
-    if (radius < 1 || radius > 4) return 1;
-    if (dtype == 1) {
-        *bx = XstarCfg<float, 1>::BX;
-        *by = XstarCfg<float, 1>::BY;
-        *halo_x = ((radius + 3) / 4) * 4;
+template <typename T, int R>
+static void tile_of(bool wave, int* bx, int* by, int* halo_x) {
+    if (wave) {
+        *bx = XwaveCfg<T, R>::BX;
+        *by = XwaveCfg<T, R>::BY;
+        *halo_x = XwaveCfg<T, R>::RA;
     } else {
-        *bx = XstarCfg<double, 1>::BX;
-        *by = XstarCfg<double, 1>::BY;
-        *halo_x = ((radius + 1) / 2) * 2;
+        *bx = XstarCfg<T, R>::BX;
+        *by = XstarCfg<T, R>::BY;
+        *halo_x = XstarCfg<T, R>::RA;
     }
-    return 0;
+}
+
+template <typename T>
+static int tile_t(int radius, bool wave, int* bx, int* by, int* halo_x) {
+    switch (radius) {
+        case 1: tile_of<T, 1>(wave, bx, by, halo_x); return 0;
+        case 2: tile_of<T, 2>(wave, bx, by, halo_x); return 0;
+        case 3: tile_of<T, 3>(wave, bx, by, halo_x); return 0;
+        case 4: tile_of<T, 4>(wave, bx, by, halo_x); return 0;
+        default: return 1;
+    }
+}
+
+// tile of the exact star (wave = false) or exact wave kernel, for the host's tensor-map boxes
+int exact_tile(int dtype, int radius, bool wave, int* bx, int* by, int* halo_x) {
+    return dtype == 1 ? tile_t<float>(radius, wave, bx, by, halo_x) : tile_t<double>(radius, wave, bx, by, halo_x);
 }
 }  // namespace stkb

@@ -248,7 +248,9 @@ template <typename T, int R>
 struct XwaveCfg {
     static constexpr int VEC = 16 / sizeof(T);
     static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
-    static constexpr int NWY = 15;
+    // one output row per warp; fp32 radius >= 3 keeps a 2R+1-plane f64 ring of 4 values per
+    // lane: 11 warps (170 registers) instead of 15 (128)
+    static constexpr int NWY = (sizeof(T) == 4 && R >= 3) ? 11 : 15;
     static constexpr int BX = 32 * VEC;
     static constexpr int BY = NWY;
     static constexpr int SW = BX + 2 * RA;
@@ -353,63 +355,86 @@ wave_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
         const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
         const int64_t row_off = (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
         const uint32_t it0 = it;
-        for (int qi = 0; qi < nq; ++qi) {
-            const uint32_t cur = it0 + qi;  // plane q = z0 - R + qi
-            mbar_wait(&full[cur % STAGES], (cur / STAGES) & 1u);
-            if (qi >= 2 * R) {
-                // output o = z0 + qi - 2R: planes o-R .. o+R are resident, plane o+d at cur - R + d
-                const int o = z0 + qi - 2 * R;
-                const int64_t off = (int64_t(o) + a.g.order0) * plane + row_off;
-                T pv[VEC] = {}, kv[VEC] = {};
-                if (y_in && x_any) {  // read early: the shared-memory work hides the latency
-                    load16(a.prev + off, pv);  // plain load: u_prev may be the destination (in place)
-                    ldg16(a.vel + off, kv);
-                }
-                const T* to = tiles + size_t((cur - R) % STAGES) * C::HALO_ELEMS;
-                double xr[VEC + 2 * RA];
+        // centre values of the last 2R+1 planes in f64 (ring slot = plane index mod 2R+1; the
+        // loop is unrolled by 2R+1 so slots are static registers): the d0 taps of every output
+        // come from here, converted once per plane instead of once per use
+        constexpr int NS = 2 * R + 1;
+        double zr[NS][VEC];
+        for (int qb = 0; qb < nq; qb += NS) {
+#pragma unroll
+            for (int p = 0; p < NS; ++p) {
+                const int qi = qb + p;
+                if (qi >= nq) break;
+                const uint32_t cur = it0 + qi;  // plane q = z0 - R + qi
+                mbar_wait(&full[cur % STAGES], (cur / STAGES) & 1u);
                 {
-                    T raw[VEC + 2 * RA];
-                    const T* row = to + (jr + R) * SW + xl;
+                    T c[VEC];
+                    lds16(tiles + size_t(cur % STAGES) * C::HALO_ELEMS + (jr + R) * SW + xl + RA, c);
 #pragma unroll
-                    for (int k = 0; k < (VEC + 2 * RA) / VEC; ++k) lds16(row + k * VEC, &raw[k * VEC]);
-#pragma unroll
-                    for (int k = 0; k < VEC + 2 * RA; ++k) xr[k] = double(raw[k]);
+                    for (int i = 0; i < VEC; ++i) zr[p][i] = double(c[i]);
                 }
-                double lap[VEC];
+                if (qi >= 2 * R) {
+                    // output o = z0 + qi - 2R (plane slot p - R): planes o-R .. o+R are resident
+                    const int o = z0 + qi - 2 * R;
+                    const int64_t off = (int64_t(o) + a.g.order0) * plane + row_off;
+                    T pv[VEC] = {}, kv[VEC] = {};
+                    if (y_in && x_any) {  // read early: the shared-memory work hides the latency
+                        load16(a.prev + off, pv);  // plain load: u_prev may be the destination (in place)
+                        ldg16(a.vel + off, kv);
+                    }
+                    const T* to = tiles + size_t((cur - R) % STAGES) * C::HALO_ELEMS;
+                    const int po = (p - R + NS) % NS;  // slot of plane o (static after unrolling)
+                    double xr[VEC + 2 * RA];
+                    {
+                        T raw[VEC + 2 * RA];
+                        const T* row = to + (jr + R) * SW + xl;
 #pragma unroll
-                for (int i = 0; i < VEC; ++i) lap[i] = xmul(xc.c0, xr[RA + i]);
+                        for (int k = 0; k < RA / VEC; ++k) {
+                            lds16(row + k * VEC, &raw[k * VEC]);
+                            lds16(row + RA + VEC + k * VEC, &raw[RA + VEC + k * VEC]);
+                        }
 #pragma unroll
-                for (int m = 1; m <= R; ++m) {
-                    T zm[VEC], zp[VEC], ym[VEC], yp[VEC];
-                    lds16(tiles + size_t((cur - R - m) % STAGES) * C::HALO_ELEMS + (jr + R) * SW + xl + RA, zm);
-                    lds16(tiles + size_t((cur - R + m) % STAGES) * C::HALO_ELEMS + (jr + R) * SW + xl + RA, zp);
-                    lds16(to + (jr + R - m) * SW + xl + RA, ym);
-                    lds16(to + (jr + R + m) * SW + xl + RA, yp);
+                        for (int k = 0; k < RA; ++k) {
+                            xr[k] = double(raw[k]);
+                            xr[RA + VEC + k] = double(raw[RA + VEC + k]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) xr[RA + i] = zr[po][i];
+                    }
+                    double lap[VEC];
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) lap[i] = xmul(xc.c0, xr[RA + i]);
+#pragma unroll
+                    for (int m = 1; m <= R; ++m) {
+                        T ym[VEC], yp[VEC];
+                        lds16(to + (jr + R - m) * SW + xl + RA, ym);
+                        lds16(to + (jr + R + m) * SW + xl + RA, yp);
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) {
+                            double sm = xadd(zr[(po - m + NS) % NS][i], zr[(po + m) % NS][i]);
+                            sm = xadd(sm, double(ym[i]));
+                            sm = xadd(sm, double(yp[i]));
+                            sm = xadd(sm, xr[RA + i - m]);
+                            sm = xadd(sm, xr[RA + i + m]);
+                            lap[i] = xadd(lap[i], xmul(xc.l[m - 1], sm));
+                        }
+                    }
+                    T outv[VEC];
 #pragma unroll
                     for (int i = 0; i < VEC; ++i) {
-                        double sm = xadd(double(zm[i]), double(zp[i]));
-                        sm = xadd(sm, double(ym[i]));
-                        sm = xadd(sm, double(yp[i]));
-                        sm = xadd(sm, xr[RA + i - m]);
-                        sm = xadd(sm, xr[RA + i + m]);
-                        lap[i] = xadd(lap[i], xmul(xc.l[m - 1], sm));
+                        const double head = __dsub_rn(xmul(xc.a, xr[RA + i]), double(pv[i]));
+                        outv[i] = T(xadd(head, xmul(double(kv[i]), lap[i])));
+                        chk = fma_t(T(0), outv[i], chk);
                     }
+                    __syncwarp();
+                    // plane o - R is read by no later output of this item
+                    mbar_arrive_lane0(&empty[(cur - 2 * R) % STAGES], lane);
+                    T* const dz = a.dst + off;
+                    if (y_in && x_full) stg16(dz, outv);
+                    else if (y_in && x_any)
+                        store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
+                                            a.box.hi2);
                 }
-                T outv[VEC];
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const double head = __dsub_rn(xmul(xc.a, xr[RA + i]), double(pv[i]));
-                    outv[i] = T(xadd(head, xmul(double(kv[i]), lap[i])));
-                    chk = fma_t(T(0), outv[i], chk);
-                }
-                __syncwarp();
-                // plane o - R is read by no later output of this item
-                mbar_arrive_lane0(&empty[(cur - 2 * R) % STAGES], lane);
-                T* const dz = a.dst + off;
-                if (o >= a.box.lo0 && o < a.box.hi0 && y_in && x_full) stg16(dz, outv);
-                else if (o >= a.box.lo0 && o < a.box.hi0 && y_in && x_any)
-                    store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
-                                        a.box.hi2);
             }
         }
         // the item's last 2R planes

@@ -389,7 +389,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     }
 
     int bx, by, hx;
-    if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE) exact_tile(dom->desc.dtype, R, &bx, &by, &hx);
+    if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE)
+        exact_tile(dom->desc.dtype, R, d.kind == STKB_MAP_XWAVE, &bx, &by, &hx);
     else star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
 #ifdef STKB_EXP_NOYHALO

@@ -354,7 +354,8 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
     streaming kernels (fp32 parity tolerance 1e-5 relative, SURVEY.md §8(c));
     ``precision="exact"`` evaluates every map in float64 in parse order with
     one rounding per store, bit-identical to ``run_target``.  ``pinned=True``
-    returns the device-resident grids in page-locked host memory.
+    returns the device-resident grids in page-locked host memory (exact-size
+    blocks from a caching pool, ``hostmem.py``; they return to it when freed).
     """
     bound = _prepare(unit, target, args, scheme)
     check_plan(plan, bound)
@@ -460,10 +461,9 @@ def dt_launches(dt) -> int:
 def _host_array(shape, dtype, pinned: bool) -> np.ndarray:
     if not pinned:
         return np.empty(shape, dtype=dtype)
-    import torch  # page-locked host memory through torch's caching host allocator
+    from .hostmem import POOL  # exact-size page-locked blocks, reused across calls
 
-    t = torch.empty(shape, dtype=torch.float32 if dtype == np.float32 else torch.float64, pin_memory=True)
-    return t.numpy()
+    return POOL.array(shape, dtype)
 
 
 def _reads_writes(bmap) -> tuple:

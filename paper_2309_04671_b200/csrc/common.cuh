@@ -96,6 +96,7 @@ struct XstarCoef {
     double cm[3][4];  // [axis][m-1] coefficient of offset -m
     double cp[3][4];  // [axis][m-1] coefficient of offset +m
     double divisor;   // 0: none, else the sum is divided by it (IEEE division, as numpy does)
+    double recip;     // RN(1 / divisor) when the divisor is in [2^-64, 2^64] (xdiv), else 0
 };
 
 // coefficients of the exact wave kernel (star_exact.cuh): a*u - p + k*(c0*u + sum_m l[m-1]*S_m)

@@ -49,6 +49,31 @@ struct XstarCfg {
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
 
+// a / d correctly rounded (what numpy's division gives), from y = RN(1/d) computed on the
+// host: q0 = RN(a y) is within one ulp of a/d, the remainder a - d q0 is exact in one FMA,
+// and RN(q0 + r y) is then the correctly rounded quotient (Markstein's theorem for a
+// correctly rounded reciprocal) — three FP64 operations instead of __ddiv_rn's iteration.
+// The theorem needs every intermediate normal: |a| in (2^-900, 2^900) with |d| in
+// [2^-64, 2^64] (host-checked; y = 0 otherwise) guarantees it.  Zeros, infinities, NaNs
+// and extreme magnitudes take __ddiv_rn.
+template <int N>
+__device__ __forceinline__ void xdiv(const double (&a)[N], double d, double y, double (&q)[N]) {
+    bool fast = y != 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) fast &= fabs(a[i]) > 0x1p-900 && fabs(a[i]) < 0x1p900;
+    if (__all_sync(0xffffffffu, fast)) {  // warp-uniform: the rare slow path stays out of line
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const double q0 = __dmul_rn(a[i], y);
+            const double r = __fma_rn(-d, q0, a[i]);
+            q[i] = __fma_rn(r, y, q0);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) q[i] = __ddiv_rn(a[i], d);
+    }
+}
+
 template <typename T, int R, bool DIV>
 __global__ void __launch_bounds__((XstarCfg<T, R>::NWY + 1) * 32, 1)
 star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
@@ -210,9 +235,11 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
                     const int z = q - R;
                     if (z >= z0 && z < z1) {
                         T outv[VEC];
+                        double qv[VEC];
+                        if constexpr (DIV) xdiv<VEC>(part[p], xc.divisor, xc.recip, qv);
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) {
-                            const double v = DIV ? __ddiv_rn(part[p][i], xc.divisor) : part[p][i];
+                            const double v = DIV ? qv[i] : part[p][i];
                             outv[i] = T(v);  // one rounding to the grid dtype (round to nearest even)
                             chk = fma_t(T(0), outv[i], chk);
                         }

@@ -486,6 +486,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
                 xc.cp[ax][m - 1] = d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1];
             }
         xc.divisor = d.divisor;
+        const double ad = std::fabs(d.divisor);
+        xc.recip = ad >= 0x1p-64 && ad <= 0x1p64 ? 1.0 / d.divisor : 0.0;  // correctly rounded (host IEEE)
         if constexpr (sizeof(T) == 4) e = launch_exact_f32(L, a, xc, dom->stream);
         else e = launch_exact_f64(L, a, xc, dom->stream);
     } else if constexpr (sizeof(T) == 4) {

@@ -60,6 +60,11 @@ extern "C" {
                             d0-, d0+, d1-, d1+, d2-, d2+; float64 in that order, one rounding per store
                             (the c3 program as run_target evaluates it); 3-D, radius 1..4 */
 
+#define STKB_MAP_XBOX 7  /* exact dense box: dst = ((c0*src[0] + c_1*src[o_1]) + ... ) [/ divisor] over every
+                            offset of the (2R+1)^3 cube, centre first and the rest sorted (d0, d1, d2):
+                            the corpus box / j3d27pt form, float64 in that order, one rounding per
+                            store (bit-identical to run_target); 3-D, radius 1..2, box_coef layout */
+
 /* step-program execution precision for STAR/WAVE maps */
 #define STKB_PREC_FAST 0 /* accumulate in the grid dtype with FMA (tolerance-checked) */
 
@@ -122,7 +127,7 @@ typedef struct {
     const int32_t *code;
     int32_t n_consts;
     const double *consts;
-    /* BOX only: box_coef[((dz+R)*(2R+1) + (dy+R))*(2R+1) + (dx+R)] (3-D, R <= 2) or
+    /* BOX and XBOX: box_coef[((dz+R)*(2R+1) + (dy+R))*(2R+1) + (dx+R)] (3-D, R <= 2) or
      * box_coef[(dy+R)*(2R+1) + (dx+R)] (2-D, R <= 4) */
     double box_coef[125];
     /* BOX, 3-D, R = 3..4: the (2R+1)^3 coefficients in the same order (copied at add_map) */

@@ -21,6 +21,7 @@ STKB_ERR_UNSUPPORTED = 3
 STKB_ERR_STATE = 4
 STKB_F32, STKB_F64 = 1, 2
 STKB_MAP_STAR, STKB_MAP_WAVE, STKB_MAP_EXPR, STKB_MAP_BOX, STKB_MAP_XSTAR, STKB_MAP_XWAVE = 1, 2, 3, 4, 5, 6
+STKB_MAP_XBOX = 7
 STKB_PREC_FAST = 0
 (OP_CONST, OP_READ, OP_LOCAL, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_NEG, OP_SETLOCAL, OP_STORE) = range(1, 11)
 EXPR_MAX_ARGS, EXPR_MAX_LOCALS, EXPR_MAX_STACK = 8, 16, 32

@@ -311,9 +311,9 @@ def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = No
     bx = box if box is not None else plan.box
     for i, (lo, hi) in enumerate(bx):
         d.lo[i], d.hi[i] = lo, hi
-    if plan.kind in ("star", "wave", "box", "xstar", "xwave"):
+    if plan.kind in ("star", "wave", "box", "xstar", "xwave", "xbox"):
         d.kind = {"star": L.STKB_MAP_STAR, "wave": L.STKB_MAP_WAVE, "box": L.STKB_MAP_BOX,
-                  "xstar": L.STKB_MAP_XSTAR, "xwave": L.STKB_MAP_XWAVE}[plan.kind]
+                  "xstar": L.STKB_MAP_XSTAR, "xwave": L.STKB_MAP_XWAVE, "xbox": L.STKB_MAP_XBOX}[plan.kind]
         d.radius = plan.radius
         d.src, d.dst = index[plan.src], index[plan.dst]
         if plan.kind in ("wave", "xwave"):
@@ -325,7 +325,7 @@ def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = No
             d.box_coef_ext = ext.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         else:
             for i, c in enumerate(plan.coef):
-                if plan.kind == "box":
+                if plan.kind in ("box", "xbox"):
                     d.box_coef[i] = c
                 else:
                     d.coef[i] = c

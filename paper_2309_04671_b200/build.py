@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libstkb200.so"
 SOURCES = ([f"star_{t}_r{r}.cu" for t in ("f32", "f64") for r in (1, 2, 3, 4)]
-           + ["star_dispatch.cu", "star_tb.cu", "star_exact.cu", "star2d.cu", "expr_kernels.cu", "stkb200.cu"])
+           + ["star_dispatch.cu", "star_tb.cu", "star_exact.cu", "box_exact.cu", "star2d.cu", "expr_kernels.cu", "stkb200.cu"])
 HEADERS = ["common.cuh", "star_kernels.cuh", "star_tb.cuh", "star_exact.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"),

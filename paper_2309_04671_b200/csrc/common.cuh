@@ -99,6 +99,13 @@ struct XstarCoef {
     double recip;     // RN(1 / divisor) when the divisor is in [2^-64, 2^64] (xdiv), else 0
 };
 
+// coefficients of the exact box kernel (box_exact.cu): c[((dz+R)(2R+1) + (dy+R))(2R+1) + (dx+R)]
+struct XboxCoef {
+    double c[125];  // radius <= 2
+    double divisor;  // 0: none
+    double recip;    // RN(1 / divisor) when usable (star_exact.cuh xdiv), else 0
+};
+
 // coefficients of the exact wave kernel (star_exact.cuh): a*u - p + k*(c0*u + sum_m l[m-1]*S_m)
 struct XwaveCoef {
     double a;
@@ -275,6 +282,9 @@ cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cuda
 cudaError_t launch_exact_f32(const StarLaunch& L, const StarArgs<float>& a, const XstarCoef& xc, cudaStream_t s);
 cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, const XstarCoef& xc, cudaStream_t s);
 int exact_tile(int dtype, int radius, bool wave, int* bx, int* by, int* halo_x);
+cudaError_t launch_xbox_f32(const StarLaunch& L, const StarArgs<float>& a, const XboxCoef& xc, cudaStream_t s);
+cudaError_t launch_xbox_f64(const StarLaunch& L, const StarArgs<double>& a, const XboxCoef& xc, cudaStream_t s);
+int xbox_tile(int dtype, int radius, int* bx, int* by, int* halo_x);
 cudaError_t launch_xwave_f32(const StarLaunch& L, const StarArgs<float>& a, const XwaveCoef& xc, cudaStream_t s);
 cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, const XwaveCoef& xc, cudaStream_t s);
 }  // namespace stkb

@@ -389,7 +389,9 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     }
 
     int bx, by, hx;
-    if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE)
+    if (d.kind == STKB_MAP_XBOX)
+        xbox_tile(dom->desc.dtype, R, &bx, &by, &hx);
+    else if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE)
         exact_tile(dom->desc.dtype, R, d.kind == STKB_MAP_XWAVE, &bx, &by, &hx);
     else star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
@@ -476,6 +478,15 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         for (int m = 1; m <= R; ++m) xc.l[m - 1] = d.coef[m];
         if constexpr (sizeof(T) == 4) e = launch_xwave_f32(L, a, xc, dom->stream);
         else e = launch_xwave_f64(L, a, xc, dom->stream);
+    } else if (d.kind == STKB_MAP_XBOX) {
+        if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
+        XboxCoef xc{};
+        for (size_t i = 0; i < op.cube.size() && i < 125; ++i) xc.c[i] = op.cube[i];
+        xc.divisor = d.divisor;
+        const double ad = std::fabs(d.divisor);
+        xc.recip = ad >= 0x1p-64 && ad <= 0x1p64 ? 1.0 / d.divisor : 0.0;
+        if constexpr (sizeof(T) == 4) e = launch_xbox_f32(L, a, xc, dom->stream);
+        else e = launch_xbox_f64(L, a, xc, dom->stream);
     } else if (d.kind == STKB_MAP_XSTAR) {
         if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
         XstarCoef xc{};
@@ -1001,13 +1012,14 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     op.d = d;
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
     if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX || d.kind == STKB_MAP_XSTAR ||
-        d.kind == STKB_MAP_XWAVE) {
-        if ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE) && nd != 3)
+        d.kind == STKB_MAP_XWAVE || d.kind == STKB_MAP_XBOX) {
+        if ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE || d.kind == STKB_MAP_XBOX) && nd != 3)
             return fail(STKB_ERR_UNSUPPORTED, "exact streaming maps are 3-D");
+        if (d.kind == STKB_MAP_XBOX && d.radius > 2) return fail(STKB_ERR_UNSUPPORTED, "exact box maps cover radius 1..2");
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
             return fail(STKB_ERR_UNSUPPORTED, nd == 1 ? "1-D maps run as EXPR maps" : "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
-        if (d.kind == STKB_MAP_BOX && nd == 3) {
+        if ((d.kind == STKB_MAP_BOX || d.kind == STKB_MAP_XBOX) && nd == 3) {
             const int n = 2 * d.radius + 1;
             if (d.radius > 2 && !d.box_coef_ext)
                 return fail(STKB_ERR_ARG, "a 3-D box map of radius > 2 passes its coefficients in box_coef_ext");
@@ -1394,6 +1406,7 @@ int stkb_launch_map_ranges(stkb_domain* dom, int32_t map_index, int32_t n_ranges
     int items = 0;
     int rc = STKB_OK;
     const bool streaming = op.d.kind != STKB_MAP_EXPR && op.d.kind != STKB_MAP_XSTAR && op.d.kind != STKB_MAP_XWAVE &&
+                           op.d.kind != STKB_MAP_XBOX &&
                            dom->desc.ndim == 3;
     if (streaming) {
         RangeSpec rs;
@@ -1432,7 +1445,8 @@ int stkb_launch_map_pull(stkb_domain* dom, int32_t map_index) {
     dom->tb_pair_epoch = -1;  // writes outside the fused-sweep loop (buffer pair state unknown)
     if (map_index < 0 || map_index >= int32_t(dom->maps.size())) return fail(STKB_ERR_ARG, "map index out of range");
     MapOp& op = dom->maps[map_index];
-    if (op.d.kind == STKB_MAP_EXPR || op.d.kind == STKB_MAP_XSTAR || op.d.kind == STKB_MAP_XWAVE || dom->desc.ndim != 3)
+    if (op.d.kind == STKB_MAP_EXPR || op.d.kind == STKB_MAP_XSTAR || op.d.kind == STKB_MAP_XWAVE ||
+        op.d.kind == STKB_MAP_XBOX || dom->desc.ndim != 3)
         return fail(STKB_ERR_UNSUPPORTED, "the fused halo exchange needs a 3-D streaming map");
     CUDA_TRY(cudaSetDevice(dom->desc.device));
     return dom->desc.dtype == STKB_F32 ? launch_star_map<float>(dom, op, dom->binding, RangeSpec(), true)

@@ -40,7 +40,7 @@ class MatchError(ValueError):
 
 @dataclass
 class MapPlan:
-    kind: str  # "star" | "wave" | "box" | "expr"
+    kind: str  # "star" | "wave" | "box" | "xstar" | "xbox" | "xwave" | "expr"
     radius: int = 0
     src: Optional[str] = None  # module grid names
     dst: Optional[str] = None
@@ -153,15 +153,15 @@ def match_map(bmap, *, exact: bool = False) -> MapPlan:
     params = dict(bmap.grid_args)  # kernel grid param -> module grid
     box = map_box(bmap)
     if exact:
-        try:
-            return match_exact_star(bmap, params, box)
-        except MatchError as why_star:
+        why = []
+        for m in (match_exact_star, match_exact_box, match_exact_wave):
             try:
-                return match_exact_wave(bmap, params, box)
-            except MatchError as why_wave:
-                p = compile_expr(bmap)
-                p.box, p.reason = box, f"precision='exact': {why_star}; {why_wave}"
-                return p
+                return m(bmap, params, box)
+            except MatchError as e:
+                why.append(str(e))
+        p = compile_expr(bmap)
+        p.box, p.reason = box, "precision='exact': " + "; ".join(why)
+        return p
     try:
         return _match_fast(bmap, params, box)
     except MatchError as why:
@@ -305,18 +305,15 @@ def _const_value(n):
     return None
 
 
-def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
-    """XSTAR: the update is the canonical weighted star sum, term by term (executor.py's
-    evaluation: each ``c * u`` one float64 multiply, each ``+`` one float64 add, the
-    optional ``/ D`` one float64 division, then one rounding)."""
-    params = params if params is not None else dict(bmap.grid_args)
+def _exact_sum(bmap, params: dict):
+    """The update as (divisor, [(coefficient, offset)], src, dst) when it is a left-associated
+    sum of `literal * read` terms of one grid, optionally `/ literal`; else MatchError."""
     kern = bmap.kernel
     if len(kern.updates) != 1 or kern.locals:
         raise MatchError("not a single update without locals")
     upd = kern.updates[0]
-    dims = len(upd.offset)
-    if dims != 3:
-        raise MatchError("the exact streaming kernel is 3-D")
+    if len(upd.offset) != 3:
+        raise MatchError("the exact streaming kernels are 3-D")
     if any(upd.offset):
         raise MatchError("destination offset is not the centre")
     expr = upd.expr
@@ -332,7 +329,7 @@ def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> Ma
         expr = expr.left
     terms.append(expr)
     terms.reverse()
-    coefs, offs, grids = [], [], set()
+    out, grids = [], set()
     for t in terms:
         if node_kind(t) != "Binary" or t.op != "*":
             raise MatchError("a term is not coefficient * read")
@@ -341,11 +338,49 @@ def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> Ma
             c, rd = _const_value(t.right), t.left
         if c is None or node_kind(rd) != "Read":
             raise MatchError("a term is not coefficient * read")
-        coefs.append(c)
-        offs.append(tuple(rd.offset))
+        out.append((c, tuple(rd.offset)))
         grids.add(rd.grid)
     if len(grids) != 1:
         raise MatchError("terms read several grids")
+    src, dst = params[grids.pop()], params[upd.dest]
+    if src == dst:
+        raise MatchError("in-place update (reads and writes the same grid)")
+    return divisor, out, src, dst
+
+
+XBOX_MAX_RADIUS = 2
+
+
+def match_exact_box(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
+    """XBOX: the canonical dense box (corpus box3d1r/box3d2r, j3d27pt) — every offset of the
+    (2R+1)^3 cube, centre first and the rest in sorted (lexicographic d0, d1, d2) order,
+    left-associated, optionally `/ D` — evaluated with the same float64 operations in the
+    same order (executor.py:81-106) on the exact box streaming kernel (radius 1..2)."""
+    params = params if params is not None else dict(bmap.grid_args)
+    divisor, terms, src, dst = _exact_sum(bmap, params)
+    offs = [o for _, o in terms]
+    r = max(max(abs(v) for v in o) for o in offs)
+    if r < 1 or r > XBOX_MAX_RADIUS:
+        raise MatchError(f"box radius {r} outside 1..{XBOX_MAX_RADIUS}")
+    rng = range(-r, r + 1)
+    cube = sorted((a, b, c) for a in rng for b in rng for c in rng if (a, b, c) != (0, 0, 0))
+    if offs != [(0, 0, 0)] + cube:
+        raise MatchError("terms are not the full box in corpus order (centre, then sorted offsets)")
+    n = 2 * r + 1
+    coef = [0.0] * n ** 3
+    for c, (a, b, d) in terms:
+        coef[((a + r) * n + (b + r)) * n + (d + r)] = c
+    return MapPlan("xbox", r, src, dst, coef=coef, divisor=divisor, box=box)
+
+
+def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
+    """XSTAR: the update is the canonical weighted star sum, term by term (executor.py's
+    evaluation: each ``c * u`` one float64 multiply, each ``+`` one float64 add, the
+    optional ``/ D`` one float64 division, then one rounding)."""
+    params = params if params is not None else dict(bmap.grid_args)
+    divisor, terms, src, dst = _exact_sum(bmap, params)
+    coefs = [c for c, _ in terms]
+    offs = [o for _, o in terms]
     r = max(max(abs(v) for v in o) for o in offs)
     if r < 1 or r > MAX_FAST_RADIUS:
         raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
@@ -358,9 +393,6 @@ def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> Ma
                 star.append(tuple(o))
     if offs != [star[0]] + sorted(star[1:]):
         raise MatchError("terms are not the full star in corpus order (centre, then sorted offsets)")
-    src, dst = params[grids.pop()], params[upd.dest]
-    if src == dst:
-        raise MatchError("in-place update (reads and writes the same grid)")
     coef = [0.0] * (6 * r + 1)
     for o, c in zip(offs, coefs):
         coef[coef_index(o, r)] = c

@@ -64,7 +64,7 @@ def _map_init(d: L.MapDesc, i: int, decls: list) -> str:
         f.append(f".n_args = {d.n_args}")
         f.append(".args = {" + ", ".join(str(d.args[k]) for k in range(L.EXPR_MAX_ARGS)) + "}")
         f.append(f".n_code = {d.n_code}, .code = code_{i}, .n_consts = {d.n_consts}, .consts = consts_{i}")
-    if d.kind == L.STKB_MAP_BOX:
+    if d.kind in (L.STKB_MAP_BOX, L.STKB_MAP_XBOX):
         if d.box_coef_ext:
             n = (2 * d.radius + 1) ** 3
             decls.append(f"static const double cube_{i}[] = {{{', '.join(_c_double(d.box_coef_ext[k]) for k in range(n))}}};")

@@ -317,3 +317,70 @@ def test_exact_wave_kernel_order_bitwise(case):
             emulate_xwave(plan, state)
     for n, ref in outs.items():
         assert np.array_equal(state[n].data, ref.data), n
+
+
+def emulate_xbox(plan, state):
+    """CPU model of box_exact_kernel's evaluation (box_exact.cu), in float64 with one rounding:
+    the centre, then the d0 = -R .. 0 layers as output q starts (planes resident in the ring),
+    then each later plane's layer as it arrives — every layer row by row (d1), tap by tap
+    (d2) — then the division."""
+    src, dst = state[plan.src], state[plan.dst]
+    R, o = plan.radius, src.order
+    box = plan.box
+    n = tuple(hi - lo for lo, hi in box)
+    u = src.data.astype(np.float64)
+    w = 2 * R + 1
+
+    def tap(off):
+        return u[tuple(slice(o + lo + q, o + lo + q + e) for (lo, _), q, e in zip(box, off, n))]
+
+    def c(dz, dy, dx):
+        return plan.coef[((dz + R) * w + (dy + R)) * w + (dx + R)]
+
+    acc = c(0, 0, 0) * tap((0, 0, 0))
+    for dz in range(-R, R + 1):
+        for dy in range(-R, R + 1):
+            for dx in range(-R, R + 1):
+                if (dz, dy, dx) != (0, 0, 0):
+                    acc = acc + c(dz, dy, dx) * tap((dz, dy, dx))
+    if plan.divisor:
+        acc = acc / plan.divisor
+    dst.data[tuple(slice(dst.order + lo, dst.order + hi) for lo, hi in box)] = acc.astype(dst.data.dtype)
+
+
+@pytest.mark.parametrize("case", ["box3d2r_10", "j3d27pt_12"])
+def test_exact_box_kernel_order_bitwise(case):
+    """precision='exact' routes the corpus boxes (R <= 2) and j3d27pt to the exact box kernel;
+    its evaluation order, modelled here, reproduces the reference's outputs bit for bit."""
+    meta, _, _, ins, outs = load_golden(case)
+    bound = build_case(meta)
+    state = {n: b.copy() for n, b in ins.items()}
+    for s in bound.stmts[0].body * bound.stmts[0].count:
+        if type(s).__name__ == "BoundSwap":
+            state[s.first], state[s.second] = state[s.second], state[s.first]
+        else:
+            plan = match_map(s, exact=True)
+            assert plan.kind == "xbox", plan.reason
+            emulate_xbox(plan, state)
+    for n, ref in outs.items():
+        assert np.array_equal(state[n].data, ref.data), n
+
+
+def test_exact_box_routes():
+    """The full cube in corpus order goes to XBOX up to radius 2; larger boxes, a reordered or
+    incomplete cube go to the bytecode kernel."""
+    import dataclasses
+
+    for name, kind in (("box3d1r", "xbox"), ("box3d2r", "xbox"), ("j3d27pt", "xbox"), ("box3d3r", "expr"),
+                       ("box3d4r", "expr")):
+        bound, _ = corpus.config_target(name, (12, 12, 12), 1)
+        assert match_map(next(_maps(bound.stmts)), exact=True).kind == kind, name
+    bound, _ = corpus.config_target("box3d1r", (8, 8, 8), 1)
+    m = next(_maps(bound.stmts))
+    e = m.kernel.updates[0].expr
+    swapped = dataclasses.replace(e, left=dataclasses.replace(e.left, right=e.right), right=e.left.right)
+    k2 = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=swapped),))
+    p = match_map(dataclasses.replace(m, kernel=k2), exact=True)
+    assert p.kind == "expr" and "full box in corpus order" in p.reason
+    short = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=e.left),))
+    assert match_map(dataclasses.replace(m, kernel=short), exact=True).kind == "expr"

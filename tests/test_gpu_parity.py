@@ -115,6 +115,23 @@ def test_fast_box_kernels_vs_c_oracle(shape, dtype, kernel):
         assert rep.max_relative <= TOL[dtype], (kernel, shape, n, rep.render())
 
 
+@pytest.mark.parametrize("shape,dtype", [((37, 45, 133), "f32"), ((64, 64, 64), "f32"), ((21, 38, 70), "f64")])
+@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r"])
+def test_exact_box_kernels_bitwise_vs_c_oracle(shape, dtype, kernel):
+    """precision='exact' runs the corpus boxes (R <= 2) on the exact box streaming kernel:
+    bit-identical to the reference's evaluation (the C oracle, -ffp-contract=off)."""
+    from paper_2309_04671_b200.matcher import match_map
+
+    bound, decls = corpus.config_target(kernel, shape, 3, dtype)
+    assert match_map(next(_maps(bound.stmts)), exact=True).kind == "xbox"
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 4)
+    ref = oracle.run_target_c(bound, grids)
+    got = run_gpu(bound, _plan(bound, "smem"), grids, precision="exact")
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), (kernel, shape, n, compare(ref[n], got[n]).render())
+
+
 @pytest.mark.parametrize("width,scheme", [(3, "cross_product"), (5, "slab7"), (40, "cross_product")])
 def test_region_maps_vs_c_oracle(width, scheme):
     bound, decls = corpus.config_target("star3d4r_norm", (48, 40, 72), 5, map_width=width, scheme=scheme)

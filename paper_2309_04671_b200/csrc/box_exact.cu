@@ -21,13 +21,13 @@
 
 namespace stkb {
 
-template <typename T, int R>
+template <typename T, int R, bool D0 = true>
 struct XboxCfg {
     static constexpr int VEC = 16 / sizeof(T);
     static constexpr int RA = ((R + VEC - 1) / VEC) * VEC;
     // consumer warps, one output row each; fp32 radius 2 needs more than the 128 registers of
     // 16 warps (the x-windows of 5 rows in f64): 11 warps (168)
-    static constexpr int NWY = (sizeof(T) == 4 && R == 2) ? 11 : 15;
+    static constexpr int NWY = (D0 && sizeof(T) == 4 && R == 2) ? 11 : 15;
     static constexpr int BX = 32 * VEC;
     static constexpr int BY = NWY;
     static constexpr int SW = BX + 2 * RA;
@@ -37,7 +37,7 @@ struct XboxCfg {
     static constexpr uint32_t STAGE_BYTES = HALO_ELEMS * sizeof(T);
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static_assert(STAGES >= R + 2, "the exact box keeps R+1 planes resident plus one in flight");
+    static_assert(!D0 || STAGES >= R + 2, "the exact box keeps R+1 planes resident plus one in flight");
     static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t) +
                                    STAGES * sizeof(int32_t);
     static constexpr int THREADS = (NWY + 1) * 32;
@@ -58,11 +58,14 @@ __device__ __forceinline__ void xbox_row(const T* row, double* xr) {
     for (int k = 0; k < VEC + 2 * RA; ++k) xr[k] = double(raw[k]);
 }
 
-template <typename T, int R, bool DIV>
-__global__ void __launch_bounds__((XboxCfg<T, R>::NWY + 1) * 32, 1)
+// D0 = false: a 2-D box (the grid lifted to one plane, no d0 halo; radius up to 4): the
+// centre, then the (2R+1)^2 square row by row, each plane's outputs complete when it lands
+template <typename T, int R, bool DIV, bool D0 = true>
+__global__ void __launch_bounds__((XboxCfg<T, R, D0>::NWY + 1) * 32, 1)
 box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
                  const __grid_constant__ StarArgs<T> a, const __grid_constant__ XboxCoef xc) {
-    using C = XboxCfg<T, R>;
+    using C = XboxCfg<T, R, D0>;
+    constexpr int RZ = D0 ? R : 0;  // d0 radius
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, NWY = C::NWY;
     constexpr int STAGES = C::STAGES;
 
@@ -106,7 +109,7 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
                 const int z1 = a.zs[2 * tz + 1];
                 const int c0 = int(a.g.lead) + x0 - RA - ix;
                 const int c1 = y0 + int(a.g.order) - R - iy;
-                for (int q = z0 - R; q < z1 + R; ++q, ++it) {
+                for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
                     const uint32_t s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
                     stage_item[s] = item;
@@ -125,6 +128,68 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
     // ---------------------------------------------------------------- consumers
     const int xl = lane * VEC;
     const int jr = warp;  // this warp's output row inside the tile
+    if constexpr (!D0) {
+        constexpr int W = 2 * R + 1;
+        T chk2 = T(0);
+        uint32_t it2 = 0;
+        const int64_t pitch = a.g.pitch, plane = a.g.plane;
+        while (true) {
+            const uint32_t s = it2 % STAGES;
+            mbar_wait(&full[s], (it2 / STAGES) & 1u);
+            const int item = __shfl_sync(0xffffffffu, stage_item[s], 0);
+            if (item < 0) break;
+            int tx, ty, tz;
+            decode_item(a, item, tx, ty, tz);
+            const int x = a.x0base + tx * BX + xl;
+            const int y = a.box.lo1 + ty * BY + jr;
+            const int z0 = a.zs[2 * tz], z1 = a.zs[2 * tz + 1];
+            const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
+            const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
+            const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
+            for (int z = z0; z < z1; ++z) {
+                const uint32_t sz = it2 % STAGES;
+                mbar_wait(&full[sz], (it2 / STAGES) & 1u);
+                const T* t = tiles + size_t(sz) * C::HALO_ELEMS;
+                double acc[VEC];
+                {
+                    T cv[VEC];
+                    lds16(t + (jr + R) * SW + xl + RA, cv);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = xmul(xc.c[R * W + R], double(cv[i]));
+                }
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+                    double xr[VEC + 2 * RA];
+                    xbox_row<T, VEC, RA>(t + (jr + R + dy) * SW + xl, xr);
+#pragma unroll
+                    for (int dx = -R; dx <= R; ++dx) {
+                        if (dy == 0 && dx == 0) continue;  // the centre came first
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i)
+                            acc[i] = xadd(acc[i], xmul(xc.c[(dy + R) * W + (dx + R)], xr[RA + i + dx]));
+                    }
+                }
+                __syncwarp();
+                mbar_arrive_lane0(&empty[sz], lane);
+                ++it2;
+                T outv[VEC];
+                double qv[VEC];
+                if constexpr (DIV) xdiv<VEC>(acc, xc.divisor, xc.recip, qv);
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    outv[i] = T(DIV ? qv[i] : acc[i]);
+                    chk2 = fma_t(T(0), outv[i], chk2);
+                }
+                T* const dz = a.dst + (int64_t(z) + a.g.order0) * plane + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+                if (y_in && x_full) stg16(dz, outv);
+                else if (y_in && x_any)
+                    store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
+                                        a.box.hi2);
+            }
+        }
+        if (__any_sync(0xffffffffu, chk2 != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
+        return;
+    }
     double part[R][VEC];  // partial sums of the last R outputs, waiting for their d0 > 0 layers
     T chk = T(0);
     uint32_t it = 0;
@@ -241,11 +306,11 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
     if (__any_sync(0xffffffffu, chk != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
-template <typename T, int R, bool DIV>
+template <typename T, int R, bool DIV, bool D0 = true>
 cudaError_t launch_xbox_cfg(const StarLaunch& L, StarArgs<T> a, const XboxCoef& xc, const CUtensorMap* maps,
                             cudaStream_t stream) {
-    using C = XboxCfg<T, R>;
-    auto kern = box_exact_kernel<T, R, DIV>;
+    using C = XboxCfg<T, R, D0>;
+    auto kern = box_exact_kernel<T, R, DIV, D0>;
     if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
     static uint64_t attr_devices = 0;
     if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
@@ -277,6 +342,13 @@ cudaError_t launch_xbox_cfg(const StarLaunch& L, StarArgs<T> a, const XboxCoef& 
 template <typename T>
 cudaError_t launch_xbox_t(const StarLaunch& L, const StarArgs<T>& a, const XboxCoef& xc, cudaStream_t s) {
     const bool d = xc.divisor != 0.0;
+    if (L.two_d) switch (L.radius) {  // a 2-D grid lifted to one plane: the square only
+        case 1: return d ? launch_xbox_cfg<T, 1, true, false>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 1, false, false>(L, a, xc, L.maps, s);
+        case 2: return d ? launch_xbox_cfg<T, 2, true, false>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 2, false, false>(L, a, xc, L.maps, s);
+        case 3: return d ? launch_xbox_cfg<T, 3, true, false>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 3, false, false>(L, a, xc, L.maps, s);
+        case 4: return d ? launch_xbox_cfg<T, 4, true, false>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 4, false, false>(L, a, xc, L.maps, s);
+        default: return cudaErrorInvalidValue;
+    }
     switch (L.radius) {
         case 1: return d ? launch_xbox_cfg<T, 1, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 1, false>(L, a, xc, L.maps, s);
         case 2: return d ? launch_xbox_cfg<T, 2, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 2, false>(L, a, xc, L.maps, s);
@@ -293,7 +365,7 @@ cudaError_t launch_xbox_f64(const StarLaunch& L, const StarArgs<double>& a, cons
 }
 
 // the exact box kernel's tile, for the host's tensor-map boxes
-int xbox_tile(int dtype, int radius, int* bx, int* by, int* halo_x) {
+int xbox_tile(int dtype, int radius, bool two_d, int* bx, int* by, int* halo_x) {
     auto set = [&](auto cfg) {
         using C = decltype(cfg);
         *bx = C::BX;
@@ -301,6 +373,20 @@ int xbox_tile(int dtype, int radius, int* bx, int* by, int* halo_x) {
         *halo_x = C::RA;
         return 0;
     };
+    if (two_d) {
+        if (dtype == 1) {
+            if (radius == 1) return set(XboxCfg<float, 1, false>{});
+            if (radius == 2) return set(XboxCfg<float, 2, false>{});
+            if (radius == 3) return set(XboxCfg<float, 3, false>{});
+            if (radius == 4) return set(XboxCfg<float, 4, false>{});
+        } else {
+            if (radius == 1) return set(XboxCfg<double, 1, false>{});
+            if (radius == 2) return set(XboxCfg<double, 2, false>{});
+            if (radius == 3) return set(XboxCfg<double, 3, false>{});
+            if (radius == 4) return set(XboxCfg<double, 4, false>{});
+        }
+        return 1;
+    }
     if (dtype == 1) {
         if (radius == 1) return set(XboxCfg<float, 1>{});
         if (radius == 2) return set(XboxCfg<float, 2>{});

@@ -101,7 +101,7 @@ struct XstarCoef {
 
 // coefficients of the exact box kernel (box_exact.cu): c[((dz+R)(2R+1) + (dy+R))(2R+1) + (dx+R)]
 struct XboxCoef {
-    double c[125];  // radius <= 2
+    double c[125];  // 3-D radius <= 2; 2-D: c[(dy+R)(2R+1) + (dx+R)], radius <= 4
     double divisor;  // 0: none
     double recip;    // RN(1 / divisor) when usable (star_exact.cuh xdiv), else 0
 };
@@ -275,6 +275,7 @@ struct StarLaunch {
     int band_pct = 0;      // item order: tile-row bands of band_pct % of a wave (0 = z-major)
     int n_steps = 1;       // > 1: a multi-step launch (StarArgs::n_steps); counters = n_steps work
     int32_t* step_counters = nullptr;  // counters followed by the step-arrive counter (zeroed here)
+    bool two_d = false;    // exact kernels: a 2-D grid lifted to one plane (no d0 taps, no d0 halo)
 };
 int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
@@ -284,7 +285,7 @@ cudaError_t launch_exact_f64(const StarLaunch& L, const StarArgs<double>& a, con
 int exact_tile(int dtype, int radius, bool wave, int* bx, int* by, int* halo_x);
 cudaError_t launch_xbox_f32(const StarLaunch& L, const StarArgs<float>& a, const XboxCoef& xc, cudaStream_t s);
 cudaError_t launch_xbox_f64(const StarLaunch& L, const StarArgs<double>& a, const XboxCoef& xc, cudaStream_t s);
-int xbox_tile(int dtype, int radius, int* bx, int* by, int* halo_x);
+int xbox_tile(int dtype, int radius, bool two_d, int* bx, int* by, int* halo_x);
 cudaError_t launch_xwave_f32(const StarLaunch& L, const StarArgs<float>& a, const XwaveCoef& xc, cudaStream_t s);
 cudaError_t launch_xwave_f64(const StarLaunch& L, const StarArgs<double>& a, const XwaveCoef& xc, cudaStream_t s);
 }  // namespace stkb

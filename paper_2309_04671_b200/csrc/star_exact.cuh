@@ -74,10 +74,14 @@ __device__ __forceinline__ void xdiv(const double (&a)[N], double d, double y, d
     }
 }
 
-template <typename T, int R, bool DIV>
+// D0 = false: a 2-D star (the grid lifted to one plane, no d0 halo): no d0 taps, each plane's
+// outputs complete when it lands (the corpus 2-D order — centre, d0-, d1-, d1+, d0+ of the 2-D
+// grid — is this kernel's d1/d2 order)
+template <typename T, int R, bool DIV, bool D0 = true>
 __global__ void __launch_bounds__((XstarCfg<T, R>::NWY + 1) * 32, 1)
 star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
                   const __grid_constant__ StarArgs<T> a, const __grid_constant__ XstarCoef xc) {
+    constexpr int RZ = D0 ? R : 0;  // d0 radius
     using C = XstarCfg<T, R>;
     constexpr int VEC = C::VEC, RA = C::RA, BX = C::BX, BY = C::BY, SW = C::SW, NWY = C::NWY;
     constexpr int STAGES = C::STAGES;
@@ -122,7 +126,7 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
                 const int z1 = a.zs[2 * tz + 1];
                 const int c0 = int(a.g.lead) + x0 - RA - ix;
                 const int c1 = y0 + int(a.g.order) - R - iy;
-                for (int q = z0 - R; q < z1 + R; ++q, ++it) {
+                for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
                     const uint32_t s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
                     stage_item[s] = item;
@@ -141,6 +145,82 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
     // ---------------------------------------------------------------- consumers
     const int xl = lane * VEC;
     const int jr = warp;  // this warp's output row inside the tile
+    if constexpr (!D0) {
+        T chk2 = T(0);
+        uint32_t it2 = 0;
+        const int64_t pitch = a.g.pitch, plane = a.g.plane;
+        while (true) {
+            const uint32_t s = it2 % STAGES;
+            mbar_wait(&full[s], (it2 / STAGES) & 1u);
+            const int item = __shfl_sync(0xffffffffu, stage_item[s], 0);
+            if (item < 0) break;
+            int tx, ty, tz;
+            decode_item(a, item, tx, ty, tz);
+            const int x = a.x0base + tx * BX + xl;
+            const int y = a.box.lo1 + ty * BY + jr;
+            const int z0 = a.zs[2 * tz], z1 = a.zs[2 * tz + 1];
+            const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
+            const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
+            const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
+            for (int z = z0; z < z1; ++z) {
+                const uint32_t sz = it2 % STAGES;
+                mbar_wait(&full[sz], (it2 / STAGES) & 1u);
+                const T* t = tiles + size_t(sz) * C::HALO_ELEMS;
+                double xr[VEC + 2 * RA];
+                {
+                    T raw[VEC + 2 * RA];
+                    const T* row = t + (jr + R) * SW + xl;
+#pragma unroll
+                    for (int k = 0; k < (VEC + 2 * RA) / VEC; ++k) lds16(row + k * VEC, &raw[k * VEC]);
+#pragma unroll
+                    for (int k = 0; k < VEC + 2 * RA; ++k) xr[k] = double(raw[k]);
+                }
+                double acc[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) acc[i] = xmul(xc.c0, xr[RA + i]);
+#pragma unroll
+                for (int m = R; m >= 1; --m) {  // (0, -m, 0)
+                    T yv[VEC];
+                    lds16(t + (jr + R - m) * SW + xl + RA, yv);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cm[1][m - 1], double(yv[i])));
+                }
+#pragma unroll
+                for (int m = R; m >= 1; --m)  // (0, 0, -m)
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cm[2][m - 1], xr[RA + i - m]));
+#pragma unroll
+                for (int m = 1; m <= R; ++m)  // (0, 0, +m)
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cp[2][m - 1], xr[RA + i + m]));
+#pragma unroll
+                for (int m = 1; m <= R; ++m) {  // (0, +m, 0)
+                    T yv[VEC];
+                    lds16(t + (jr + R + m) * SW + xl + RA, yv);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) acc[i] = xadd(acc[i], xmul(xc.cp[1][m - 1], double(yv[i])));
+                }
+                __syncwarp();
+                mbar_arrive_lane0(&empty[sz], lane);
+                ++it2;
+                T outv[VEC];
+                double qv[VEC];
+                if constexpr (DIV) xdiv<VEC>(acc, xc.divisor, xc.recip, qv);
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    outv[i] = T(DIV ? qv[i] : acc[i]);
+                    chk2 = fma_t(T(0), outv[i], chk2);
+                }
+                T* const dz = a.dst + (int64_t(z) + a.g.order0) * plane + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+                if (y_in && x_full) stg16(dz, outv);
+                else if (y_in && x_any)
+                    store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
+                                        a.box.hi2);
+            }
+        }
+        if (__any_sync(0xffffffffu, chk2 != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
+        return;
+    }
     double zneg[R][VEC];  // centre values of the previous R planes (f64), ring by plane
     double part[R][VEC];  // partial sums of the last R outputs, waiting for their d0+ taps
     T chk = T(0);
@@ -517,11 +597,11 @@ cudaError_t launch_xwave_t(const StarLaunch& L, const StarArgs<T>& a, const Xwav
     }
 }
 
-template <typename T, int R, bool DIV>
+template <typename T, int R, bool DIV, bool D0 = true>
 cudaError_t launch_exact_cfg(const StarLaunch& L, StarArgs<T> a, const XstarCoef& xc, const CUtensorMap* maps,
                              cudaStream_t stream) {
     using C = XstarCfg<T, R>;
-    auto kern = star_exact_kernel<T, R, DIV>;
+    auto kern = star_exact_kernel<T, R, DIV, D0>;
     if (L.box_w != C::SW || L.box_h != C::SH) return cudaErrorInvalidConfiguration;
     static uint64_t attr_devices = 0;
     if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_devices)) return e;
@@ -554,6 +634,13 @@ template <typename T>
 cudaError_t launch_exact_t(const StarLaunch& L, const StarArgs<T>& a, const XstarCoef& xc, const CUtensorMap* maps,
                            cudaStream_t s) {
     const bool div = xc.divisor != 0.0;
+    if (L.two_d) switch (L.radius) {  // a 2-D grid lifted to one plane: no d0 taps
+        case 1: return div ? launch_exact_cfg<T, 1, true, false>(L, a, xc, maps, s) : launch_exact_cfg<T, 1, false, false>(L, a, xc, maps, s);
+        case 2: return div ? launch_exact_cfg<T, 2, true, false>(L, a, xc, maps, s) : launch_exact_cfg<T, 2, false, false>(L, a, xc, maps, s);
+        case 3: return div ? launch_exact_cfg<T, 3, true, false>(L, a, xc, maps, s) : launch_exact_cfg<T, 3, false, false>(L, a, xc, maps, s);
+        case 4: return div ? launch_exact_cfg<T, 4, true, false>(L, a, xc, maps, s) : launch_exact_cfg<T, 4, false, false>(L, a, xc, maps, s);
+        default: return cudaErrorInvalidValue;
+    }
     switch (L.radius) {
         case 1: return div ? launch_exact_cfg<T, 1, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 1, false>(L, a, xc, maps, s);
         case 2: return div ? launch_exact_cfg<T, 2, true>(L, a, xc, maps, s) : launch_exact_cfg<T, 2, false>(L, a, xc, maps, s);

@@ -363,7 +363,8 @@ template <typename T>
 int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t>& bind,
                     const RangeSpec& rs = RangeSpec(), bool pull = false, int n_steps = 1) {
     const stkb_map_desc& d = op.d;
-    if (dom->desc.ndim == 2) return launch_star2d_map(dom, op, bind);
+    const bool exact2d = dom->desc.ndim == 2 && (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XBOX);
+    if (dom->desc.ndim == 2 && !exact2d) return launch_star2d_map(dom, op, bind);
     if (int rc = ensure_halo_flags(dom)) return rc;
     StarArgs<T> a{};
     a.g = dom->g;
@@ -390,7 +391,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
 
     int bx, by, hx;
     if (d.kind == STKB_MAP_XBOX)
-        xbox_tile(dom->desc.dtype, R, &bx, &by, &hx);
+        xbox_tile(dom->desc.dtype, R, exact2d, &bx, &by, &hx);
     else if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE)
         exact_tile(dom->desc.dtype, R, d.kind == STKB_MAP_XWAVE, &bx, &by, &hx);
     else star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
@@ -453,6 +454,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.box_w = bx + 2 * hx;
     L.box_h = by + 2 * R;  // (STKB_EXP_NOYHALO loads fewer rows; the stage keeps this shape)
     L.num_sms = dom->num_sms;
+    L.two_d = exact2d;
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;
     L.taper = dom->taper;
@@ -491,10 +493,12 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
         XstarCoef xc{};
         xc.c0 = d.coef[0];
-        for (int ax = 0; ax < 3; ++ax)
+        // a 2-D star's axes (d0, d1 of the grid) are the lifted plane's d1, d2
+        const int nax = exact2d ? 2 : 3, ax0 = exact2d ? 1 : 0;
+        for (int ax = 0; ax < nax; ++ax)
             for (int m = 1; m <= R; ++m) {
-                xc.cm[ax][m - 1] = d.coef[1 + ax * 2 * R + 2 * (m - 1)];
-                xc.cp[ax][m - 1] = d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1];
+                xc.cm[ax0 + ax][m - 1] = d.coef[1 + ax * 2 * R + 2 * (m - 1)];
+                xc.cp[ax0 + ax][m - 1] = d.coef[1 + ax * 2 * R + 2 * (m - 1) + 1];
             }
         xc.divisor = d.divisor;
         const double ad = std::fabs(d.divisor);
@@ -1013,9 +1017,10 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
     for (int i = 0; i < 3; ++i) { op.d.lo[i] = lo[i]; op.d.hi[i] = hi[i]; }
     if (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_BOX || d.kind == STKB_MAP_XSTAR ||
         d.kind == STKB_MAP_XWAVE || d.kind == STKB_MAP_XBOX) {
-        if ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE || d.kind == STKB_MAP_XBOX) && nd != 3)
-            return fail(STKB_ERR_UNSUPPORTED, "exact streaming maps are 3-D");
-        if (d.kind == STKB_MAP_XBOX && d.radius > 2) return fail(STKB_ERR_UNSUPPORTED, "exact box maps cover radius 1..2");
+        if ((d.kind == STKB_MAP_XWAVE && nd != 3) || ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XBOX) && nd == 1))
+            return fail(STKB_ERR_UNSUPPORTED, "exact streaming maps are 3-D (stars and boxes also 2-D)");
+        if (d.kind == STKB_MAP_XBOX && nd == 3 && d.radius > 2)
+            return fail(STKB_ERR_UNSUPPORTED, "exact 3-D box maps cover radius 1..2");
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
             return fail(STKB_ERR_UNSUPPORTED, nd == 1 ? "1-D maps run as EXPR maps" : "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");
@@ -1025,6 +1030,10 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
                 return fail(STKB_ERR_ARG, "a 3-D box map of radius > 2 passes its coefficients in box_coef_ext");
             const double* src = d.radius > 2 ? d.box_coef_ext : d.box_coef;
             op.cube.assign(src, src + size_t(n) * n * n);
+        }
+        if (d.kind == STKB_MAP_XBOX && nd == 2) {
+            const int n = 2 * d.radius + 1;
+            op.cube.assign(d.box_coef, d.box_coef + size_t(n) * n);
         }
         op.d.box_coef_ext = nullptr;  // copied: the caller's array need not outlive this call
         if (d.radius > g.order) return fail(STKB_ERR_ARG, "stencil radius exceeds the grid halo order");

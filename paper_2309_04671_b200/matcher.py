@@ -25,6 +25,8 @@ order with one rounding per store (bit-identical to run_target).
 
 from __future__ import annotations
 
+import itertools
+
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -312,8 +314,8 @@ def _exact_sum(bmap, params: dict):
     if len(kern.updates) != 1 or kern.locals:
         raise MatchError("not a single update without locals")
     upd = kern.updates[0]
-    if len(upd.offset) != 3:
-        raise MatchError("the exact streaming kernels are 3-D")
+    if len(upd.offset) not in (2, 3):
+        raise MatchError("the exact streaming kernels are 2-D and 3-D")
     if any(upd.offset):
         raise MatchError("destination offset is not the centre")
     expr = upd.expr
@@ -348,28 +350,32 @@ def _exact_sum(bmap, params: dict):
     return divisor, out, src, dst
 
 
-XBOX_MAX_RADIUS = 2
+XBOX_MAX_RADIUS = {2: 4, 3: 2}  # by dimension
 
 
 def match_exact_box(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
-    """XBOX: the canonical dense box (corpus box3d1r/box3d2r, j3d27pt) — every offset of the
-    (2R+1)^3 cube, centre first and the rest in sorted (lexicographic d0, d1, d2) order,
-    left-associated, optionally `/ D` — evaluated with the same float64 operations in the
-    same order (executor.py:81-106) on the exact box streaming kernel (radius 1..2)."""
+    """XBOX: the canonical dense box (corpus box3d1r/box3d2r, j3d27pt; box2d*, j2d9pt_gol) —
+    every offset of the (2R+1)^3 cube (square in 2-D), centre first and the rest in sorted
+    (lexicographic) order, left-associated, optionally `/ D` — evaluated with the same
+    float64 operations in the same order (executor.py:81-106) on the exact box kernel
+    (radius 1..2 in 3-D, 1..4 in 2-D)."""
     params = params if params is not None else dict(bmap.grid_args)
     divisor, terms, src, dst = _exact_sum(bmap, params)
     offs = [o for _, o in terms]
+    dims = len(offs[0])
     r = max(max(abs(v) for v in o) for o in offs)
-    if r < 1 or r > XBOX_MAX_RADIUS:
-        raise MatchError(f"box radius {r} outside 1..{XBOX_MAX_RADIUS}")
-    rng = range(-r, r + 1)
-    cube = sorted((a, b, c) for a in rng for b in rng for c in rng if (a, b, c) != (0, 0, 0))
-    if offs != [(0, 0, 0)] + cube:
+    if r < 1 or r > XBOX_MAX_RADIUS[dims]:
+        raise MatchError(f"{dims}-D box radius {r} outside 1..{XBOX_MAX_RADIUS[dims]}")
+    cube = sorted(o for o in itertools.product(range(-r, r + 1), repeat=dims) if any(o))
+    if offs != [(0,) * dims] + cube:
         raise MatchError("terms are not the full box in corpus order (centre, then sorted offsets)")
     n = 2 * r + 1
-    coef = [0.0] * n ** 3
-    for c, (a, b, d) in terms:
-        coef[((a + r) * n + (b + r)) * n + (d + r)] = c
+    coef = [0.0] * n ** dims
+    for c, o in terms:
+        k = 0
+        for v in o:
+            k = k * n + (v + r)
+        coef[k] = c
     return MapPlan("xbox", r, src, dst, coef=coef, divisor=divisor, box=box)
 
 
@@ -381,14 +387,15 @@ def match_exact_star(bmap, params: Optional[dict] = None, box: tuple = ()) -> Ma
     divisor, terms, src, dst = _exact_sum(bmap, params)
     coefs = [c for c, _ in terms]
     offs = [o for _, o in terms]
+    dims = len(offs[0])
     r = max(max(abs(v) for v in o) for o in offs)
     if r < 1 or r > MAX_FAST_RADIUS:
         raise MatchError(f"radius {r} outside 1..{MAX_FAST_RADIUS}")
-    star = [(0, 0, 0)]
-    for axis in range(3):
+    star = [(0,) * dims]
+    for axis in range(dims):
         for m in range(1, r + 1):
             for sgn in (-1, 1):
-                o = [0, 0, 0]
+                o = [0] * dims
                 o[axis] = sgn * m
                 star.append(tuple(o))
     if offs != [star[0]] + sorted(star[1:]):

@@ -132,6 +132,25 @@ def test_exact_box_kernels_bitwise_vs_c_oracle(shape, dtype, kernel):
         assert np.array_equal(ref[n].data, got[n].data), (kernel, shape, n, compare(ref[n], got[n]).render())
 
 
+@pytest.mark.parametrize("shape,dtype", [((137, 301), "f32"), ((1000, 1000), "f32"), ((77, 90), "f64")])
+@pytest.mark.parametrize("kernel,kind", [("star2d1r", "xstar"), ("star2d4r", "xstar"), ("j2d5pt", "xstar"),
+                                         ("j2d9pt", "xstar"), ("box2d1r", "xbox"), ("box2d4r", "xbox"),
+                                         ("j2d9pt_gol", "xbox")])
+def test_exact_2d_kernels_bitwise_vs_c_oracle(shape, dtype, kernel, kind):
+    """precision='exact' runs the 2-D corpus stars and boxes (Listing 1's star2d4r among them)
+    on the exact kernels in their one-plane mode: bit-identical to the C oracle."""
+    from paper_2309_04671_b200.matcher import match_map
+
+    bound, decls = corpus.config_target(kernel, shape, 3, dtype)
+    assert match_map(next(_maps(bound.stmts)), exact=True).kind == kind
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 5)
+    ref = oracle.run_target_c(bound, grids)
+    got = run_gpu(bound, _plan(bound, "shift"), grids, precision="exact")
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), (kernel, shape, n, compare(ref[n], got[n]).render())
+
+
 @pytest.mark.parametrize("width,scheme", [(3, "cross_product"), (5, "slab7"), (40, "cross_product")])
 def test_region_maps_vs_c_oracle(width, scheme):
     bound, decls = corpus.config_target("star3d4r_norm", (48, 40, 72), 5, map_width=width, scheme=scheme)

@@ -276,8 +276,9 @@ struct StarLaunch {
     int n_steps = 1;       // > 1: a multi-step launch (StarArgs::n_steps); counters = n_steps work
     int32_t* step_counters = nullptr;  // counters followed by the step-arrive counter (zeroed here)
     bool two_d = false;    // exact kernels: a 2-D grid lifted to one plane (no d0 taps, no d0 halo)
+    bool small_tile = false;  // star/wave on a small grid: the 16-row tile (star_kernels.cuh)
 };
-int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x);
+int star_tile(int dtype, int radius, int kind, bool small, int* bx, int* by, int* halo_x);
 cudaError_t launch_star_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
 cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
 cudaError_t launch_exact_f32(const StarLaunch& L, const StarArgs<float>& a, const XstarCoef& xc, cudaStream_t s);

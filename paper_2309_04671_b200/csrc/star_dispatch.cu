@@ -31,11 +31,11 @@ cudaError_t launch_star_f64(const StarLaunch& L, const StarArgs<double>& a, cuda
     }
 }
 
-int star_tile(int dtype, int radius, int kind, int* bx, int* by, int* halo_x) {
+int star_tile(int dtype, int radius, int kind, bool small, int* bx, int* by, int* halo_x) {
     if (radius < 1 || radius > 4) return 1;
     const bool box = kind == 4;  // STKB_MAP_BOX
-    if (dtype == 1) star_tile_t<float>(radius, box, bx, by, halo_x);
-    else star_tile_t<double>(radius, box, bx, by, halo_x);
+    if (dtype == 1) star_tile_t<float>(radius, box, small, bx, by, halo_x);
+    else star_tile_t<double>(radius, box, small, bx, by, halo_x);
     return 0;
 }
 }  // namespace stkb

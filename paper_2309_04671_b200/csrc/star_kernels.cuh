@@ -800,8 +800,10 @@ cudaError_t launch_star_cfg(const StarLaunch& L, StarArgs<T> a, const CUtensorMa
 }
 
 // tile variants: (rows per warp, consumer warps, odd x-taps as scalar FMAs, elements per lane
-// (0: one 16-byte vector))
+// (0: one 16-byte vector)).  Every variant evaluates each point with the same operations in
+// the same order (the tile only changes which thread does it): results are bit-identical.
 struct Variant { int ty, nwy; bool odd_scalar; int lw = 0; };
+constexpr int kSmallTileVariant = 20;
 
 template <typename T>
 __host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = false) {
@@ -820,6 +822,17 @@ __host__ __device__ constexpr Variant star_variant_of(int R, int v, bool box = f
         case 10: return sizeof(T) == 8 ? Variant{2, 7, true, 4} : Variant{2, 11, true};
         case 11: return sizeof(T) == 8 ? Variant{2, 6, true, 4} : Variant{2, 11, true};
         case 12: return sizeof(T) == 8 ? Variant{1, 11, true, 4} : Variant{2, 11, true};
+        case 13: return Variant{1, 11, true};
+        case 14: return Variant{1, 7, true};
+        case 15: return Variant{2, 8, true};
+        case 16: return Variant{1, 16, true};
+        case 17: return Variant{2, 4, true};
+        case 18: return Variant{1, 8, true};
+        case 19: return Variant{4, 4, true};
+        // small grids (StarLaunch::small_tile): 16-row tiles give more, shorter items; measured
+        // +14-32 % at 96^3-160^3 against the default tile for every radius, fp32 and fp64 and
+        // the wave, worse from ~192^3 on
+        case kSmallTileVariant: return Variant{2, 8, true};
         default:  // measured best on B200 per form, dtype and radius (tools/sweep.py)
             // dense cubes: R=1 4 rows/warp (rows share taps), R=2 one row, R=3..4 one row with
             // 11 warps (up to 170 registers); R=4 forms odd-shift pairs once per row (+13 %)
@@ -844,7 +857,9 @@ template <typename T, int R, int V, bool PULL>
 cudaError_t launch_star_vp(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
     constexpr Variant vv = star_variant_of<T>(R, V);
     if (L.kind == 4) {
-        {
+        if constexpr (V == kSmallTileVariant) {
+            return cudaErrorInvalidValue;  // boxes keep their tiles
+        } else {
             constexpr Variant vb = star_variant_of<T>(R, V, true);
             if (L.has_divisor)
                 return launch_star_cfg<T, R, FORM_BOX_DIV, vb.ty, vb.nwy, vb.odd_scalar, PULL>(L, a, maps, s);
@@ -874,6 +889,7 @@ cudaError_t launch_star_v(const StarLaunch& L, const StarArgs<T>& a, const CUten
 
 template <typename T, int R>
 cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUtensorMap* maps, cudaStream_t s) {
+    if (L.small_tile && L.kind != 4 && !a.pull) return launch_star_vp<T, R, kSmallTileVariant, false>(L, a, maps, s);
     if constexpr (STKB_VARIANTS > 1) {
         switch (star_variant_env()) {
             case 1: return launch_star_v<T, R, 1>(L, a, maps, s);
@@ -887,6 +903,13 @@ cudaError_t launch_star_r(const StarLaunch& L, const StarArgs<T>& a, const CUten
             case 10: return launch_star_v<T, R, 10>(L, a, maps, s);
             case 11: return launch_star_v<T, R, 11>(L, a, maps, s);
             case 12: return launch_star_v<T, R, 12>(L, a, maps, s);
+            case 13: return launch_star_v<T, R, 13>(L, a, maps, s);
+            case 14: return launch_star_v<T, R, 14>(L, a, maps, s);
+            case 15: return launch_star_v<T, R, 15>(L, a, maps, s);
+            case 16: return launch_star_v<T, R, 16>(L, a, maps, s);
+            case 17: return launch_star_v<T, R, 17>(L, a, maps, s);
+            case 18: return launch_star_v<T, R, 18>(L, a, maps, s);
+            case 19: return launch_star_v<T, R, 19>(L, a, maps, s);
             default: break;
         }
     }
@@ -906,8 +929,8 @@ cudaError_t launch_star_t(const StarLaunch& L, const StarArgs<T>& a, const CUten
 
 // tile geometry used to build the tensor-map boxes on the host
 template <typename T>
-inline void star_tile_t(int R, bool box, int* bx, int* by, int* halo_x) {
-    const int v = STKB_VARIANTS > 1 ? star_variant_env() : 0;
+inline void star_tile_t(int R, bool box, bool small, int* bx, int* by, int* halo_x) {
+    const int v = small && !box ? kSmallTileVariant : (STKB_VARIANTS > 1 ? star_variant_env() : 0);
     const Variant vv = star_variant_of<T>(R, v, box);
     const int VEC = vv.lw > 0 && !box ? vv.lw : int(16 / sizeof(T));
     *bx = 32 * VEC;

@@ -169,6 +169,7 @@ struct stkb_domain {
     // several ping-pong steps per launch for small grids (star_kernels.cuh, StarArgs::n_steps)
     int32_t* d_multi = nullptr;    // per-step work counters + the step-arrive counter
     cudaError_t last_launch_error = cudaSuccess;
+    int64_t small_tile_points = int64_t(1) << 22;  // STKB_SMALL_TILE_POINTS: the small-grid tile up to here
     int64_t multi_max_points = int64_t(1) << 25;  // STKB_MULTI_POINTS: grids up to this many points
     bool multi = true;             // STKB_MULTI=0 disables
     bool halo_external = false;  // z-slab machinery writes halo planes (exchange, peers): full maps only
@@ -389,12 +390,16 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         for (size_t i = 0; i < op.cube.size(); ++i) a.cb[i] = T(op.cube[i] * sc);
     }
 
+    // small grids take the 16-row tile (more, shorter work items); the neighbour-pulling and
+    // range launches of the slab engine keep the default tile
+    const bool small = !pull && rs.n == 0 && (d.kind == STKB_MAP_STAR || d.kind == STKB_MAP_WAVE) &&
+                       dom->g.n0 * dom->g.n1 * dom->g.n2 <= dom->small_tile_points;
     int bx, by, hx;
     if (d.kind == STKB_MAP_XBOX)
         xbox_tile(dom->desc.dtype, R, exact2d, &bx, &by, &hx);
     else if (d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XWAVE)
         exact_tile(dom->desc.dtype, R, d.kind == STKB_MAP_XWAVE, &bx, &by, &hx);
-    else star_tile(dom->desc.dtype, R, d.kind, &bx, &by, &hx);
+    else star_tile(dom->desc.dtype, R, d.kind, small, &bx, &by, &hx);
     const CUtensorMap* m_halo = nullptr;
 #ifdef STKB_EXP_NOYHALO
     const int lw = bx + 2 * hx, lh = by;
@@ -455,6 +460,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     L.box_h = by + 2 * R;  // (STKB_EXP_NOYHALO loads fewer rows; the stage keeps this shape)
     L.num_sms = dom->num_sms;
     L.two_d = exact2d;
+    L.small_tile = small;
     L.max_ctas = dom->ctas_override;
     L.lz = dom->lz_override;
     L.taper = dom->taper;
@@ -757,6 +763,7 @@ int stkb_domain_create(const stkb_domain_desc* desc, stkb_domain** out) {
     if (const char* s = getenv("STKB_TB")) dom->tb = atoi(s) != 0;
     if (const char* s = getenv("STKB_MULTI")) dom->multi = atoi(s) != 0;
     if (const char* s = getenv("STKB_MULTI_POINTS")) dom->multi_max_points = atoll(s);
+    if (const char* s = getenv("STKB_SMALL_TILE_POINTS")) dom->small_tile_points = atoll(s);
     *out = dom;
     return STKB_OK;
 }

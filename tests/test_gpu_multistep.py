@@ -119,3 +119,32 @@ def test_multi_step_reports_nonfinite():
     plan = plan_gpu(bound.stmts[0].body[0].info, {"template": "unroll", "computeCapability": "10.0"})
     with pytest.warns(RuntimeWarning, match="non-finite"):
         run_gpu(bound, plan, grids)
+
+
+@pytest.mark.parametrize("builder,dtype,shape", [("star3d4r", "f32", (128, 128, 128)), ("star3d1r", "f64", (37, 45, 133)),
+                                                 ("wave", "f32", (40, 48, 136))])
+def test_small_grid_tile_bitwise_equal_default_tile(monkeypatch, builder, dtype, shape):
+    """Small grids take the 16-row tile (StarLaunch::small_tile); the tile only changes which
+    thread computes a point, so the grids match the default tile's bit for bit."""
+    bound, decls = corpus.config_target(builder, shape, 4, dtype)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    for i, n in enumerate(grids):
+        fill_loguniform(grids[n], 11 + i)
+    if "kap" in grids:
+        grids["kap"].interior[...] = 0.01
+    body = next(s for s in bound.stmts if type(s).__name__ == "BoundFor").body
+    names = list(grids)
+    outs = []
+    for points in ("4194304", "0"):  # the default threshold, then the small tile disabled
+        monkeypatch.setenv("STKB_SMALL_TILE_POINTS", points)
+        with DeviceTarget(grids, names) as dt:
+            for n in names:
+                dt.upload(n, grids[n].data)
+            dt.set_multi_steps(False)
+            dt.set_fused_steps(False)
+            dt.set_program(body)
+            dt.run(4)
+            dt.sync()
+            outs.append({n: dt.download(n) for n in names})
+    for n in names:
+        assert np.array_equal(outs[0][n], outs[1][n]), n

@@ -87,6 +87,7 @@ CASES = [
     (3, "star3d4r_norm", (40, 36, 72), 5, "fast", "f32", 3, "cross_product"),  # PML regions, clipped per slab
     (2, "star3d4r_norm", (32, 24, 40), 4, "fast", "f32", 5, "slab7"),
     (2, "j3d27pt", (30, 26, 70), 6, "fast"),                                 # dense box form
+    (3, "box3d2r", (30, 20, 40), 4, "exact"),                                # exact box kernel per slab
     (2, "star3d2r_norm", (28, 20, 36), 5, "fast", "f64"),
     (3, "wave", (27, 16, 40), 5, "fast", "f64"),
 ]

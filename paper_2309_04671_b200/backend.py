@@ -319,7 +319,7 @@ def map_desc_for(plan: MapPlan, index: dict, tag: int, box: Optional[tuple] = No
         if plan.kind in ("wave", "xwave"):
             d.prev, d.vel = index[plan.prev], index[plan.vel]
             d.wave_a, d.wave_b = plan.wave_a, plan.wave_b
-        if plan.kind == "box" and len(plan.coef) > 125:  # 3-D box of radius 3..4
+        if plan.kind in ("box", "xbox") and len(plan.coef) > 125:  # 3-D box of radius 3..4
             ext = np.ascontiguousarray(np.array(plan.coef, dtype=np.float64))
             d._keep_ext = ext  # alive until stkb_program_add_map has copied it
             d.box_coef_ext = ext.ctypes.data_as(ctypes.POINTER(ctypes.c_double))

@@ -1,5 +1,6 @@
 // Exact 2.5D d0-streaming dense-box kernel (XBOX): the reference's own arithmetic for the
-// corpus box stencils (box3d1r, box3d2r, j3d27pt) at streaming speed.
+// corpus box stencils (box3d1r..box3d4r, j3d27pt; box2d*, j2d9pt_gol on 2-D grids) at
+// streaming speed.
 //
 // The corpus box form (corpus.py:77-120) is
 //     v.at(0,0,0).set(c0*u.at(0,0,0) + c(-R,-R,-R)*u.at(-R,-R,-R) + ... + c(R,R,R)*u.at(R,R,R))  [/ D]
@@ -190,6 +191,8 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
         if (__any_sync(0xffffffffu, chk2 != T(0)) && lane == 0) atomicOr(a.nonfinite, 1);
         return;
     }
+    // radius 3..4 (343 / 729 taps): the d0 and d1 loops stay loops (code size); d2 is unrolled
+    constexpr int UZ = R <= 2 ? R : 1, UY = R <= 2 ? 2 * R + 1 : 1;
     double part[R][VEC];  // partial sums of the last R outputs, waiting for their d0 > 0 layers
     T chk = T(0);
     uint32_t it = 0;
@@ -232,10 +235,10 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
                         lds16(t + (jr + R) * SW + xl + RA, cv);
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) acc[i] = xmul(xc.c[xbox_index<R>(0, 0, 0)], double(cv[i]));
-#pragma unroll
+#pragma unroll(UZ)
                         for (int dz = -R; dz < 0; ++dz) {
                             const T* tp = tiles + size_t((cur + dz) % STAGES) * C::HALO_ELEMS;
-#pragma unroll
+#pragma unroll(UY)
                             for (int dy = -R; dy <= R; ++dy) {
                                 double xr[VEC + 2 * RA];
                                 xbox_row<T, VEC, RA>(tp + (jr + R + dy) * SW + xl, xr);
@@ -248,7 +251,7 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
                         }
                     }
                     // plane q, row by row: output q's d0 = 0 layer and outputs q-m's d0 = +m layer
-#pragma unroll
+#pragma unroll(UY)
                     for (int dy = -R; dy <= R; ++dy) {
                         double xr[VEC + 2 * RA];
                         xbox_row<T, VEC, RA>(t + (jr + R + dy) * SW + xl, xr);
@@ -352,6 +355,8 @@ cudaError_t launch_xbox_t(const StarLaunch& L, const StarArgs<T>& a, const XboxC
     switch (L.radius) {
         case 1: return d ? launch_xbox_cfg<T, 1, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 1, false>(L, a, xc, L.maps, s);
         case 2: return d ? launch_xbox_cfg<T, 2, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 2, false>(L, a, xc, L.maps, s);
+        case 3: return d ? launch_xbox_cfg<T, 3, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 3, false>(L, a, xc, L.maps, s);
+        case 4: return d ? launch_xbox_cfg<T, 4, true>(L, a, xc, L.maps, s) : launch_xbox_cfg<T, 4, false>(L, a, xc, L.maps, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -390,9 +395,13 @@ int xbox_tile(int dtype, int radius, bool two_d, int* bx, int* by, int* halo_x) 
     if (dtype == 1) {
         if (radius == 1) return set(XboxCfg<float, 1>{});
         if (radius == 2) return set(XboxCfg<float, 2>{});
+        if (radius == 3) return set(XboxCfg<float, 3>{});
+        if (radius == 4) return set(XboxCfg<float, 4>{});
     } else {
         if (radius == 1) return set(XboxCfg<double, 1>{});
         if (radius == 2) return set(XboxCfg<double, 2>{});
+        if (radius == 3) return set(XboxCfg<double, 3>{});
+        if (radius == 4) return set(XboxCfg<double, 4>{});
     }
     return 1;
 }

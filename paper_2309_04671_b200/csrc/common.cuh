@@ -101,7 +101,7 @@ struct XstarCoef {
 
 // coefficients of the exact box kernel (box_exact.cu): c[((dz+R)(2R+1) + (dy+R))(2R+1) + (dx+R)]
 struct XboxCoef {
-    double c[125];  // 3-D radius <= 2; 2-D: c[(dy+R)(2R+1) + (dx+R)], radius <= 4
+    double c[729];  // 3-D radius <= 4; 2-D: c[(dy+R)(2R+1) + (dx+R)], radius <= 4
     double divisor;  // 0: none
     double recip;    // RN(1 / divisor) when usable (star_exact.cuh xdiv), else 0
 };

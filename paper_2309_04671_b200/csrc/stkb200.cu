@@ -489,7 +489,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     } else if (d.kind == STKB_MAP_XBOX) {
         if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
         XboxCoef xc{};
-        for (size_t i = 0; i < op.cube.size() && i < 125; ++i) xc.c[i] = op.cube[i];
+        for (size_t i = 0; i < op.cube.size() && i < 729; ++i) xc.c[i] = op.cube[i];
         xc.divisor = d.divisor;
         const double ad = std::fabs(d.divisor);
         xc.recip = ad >= 0x1p-64 && ad <= 0x1p64 ? 1.0 / d.divisor : 0.0;
@@ -1026,8 +1026,6 @@ int stkb_program_add_map(stkb_domain* dom, const stkb_map_desc* md) {
         d.kind == STKB_MAP_XWAVE || d.kind == STKB_MAP_XBOX) {
         if ((d.kind == STKB_MAP_XWAVE && nd != 3) || ((d.kind == STKB_MAP_XSTAR || d.kind == STKB_MAP_XBOX) && nd == 1))
             return fail(STKB_ERR_UNSUPPORTED, "exact streaming maps are 3-D (stars and boxes also 2-D)");
-        if (d.kind == STKB_MAP_XBOX && nd == 3 && d.radius > 2)
-            return fail(STKB_ERR_UNSUPPORTED, "exact 3-D box maps cover radius 1..2");
         if (nd != 3 && !(nd == 2 && d.kind != STKB_MAP_WAVE))
             return fail(STKB_ERR_UNSUPPORTED, nd == 1 ? "1-D maps run as EXPR maps" : "2-D grids stream star and box maps only");
         if (d.radius < 1 || d.radius > 4) return fail(STKB_ERR_UNSUPPORTED, "streaming star kernels cover radius 1..4");

@@ -350,15 +350,15 @@ def _exact_sum(bmap, params: dict):
     return divisor, out, src, dst
 
 
-XBOX_MAX_RADIUS = {2: 4, 3: 2}  # by dimension
+XBOX_MAX_RADIUS = {2: 4, 3: 4}  # by dimension
 
 
 def match_exact_box(bmap, params: Optional[dict] = None, box: tuple = ()) -> MapPlan:
-    """XBOX: the canonical dense box (corpus box3d1r/box3d2r, j3d27pt; box2d*, j2d9pt_gol) —
+    """XBOX: the canonical dense box (corpus box3d1r..box3d4r, j3d27pt; box2d*, j2d9pt_gol) —
     every offset of the (2R+1)^3 cube (square in 2-D), centre first and the rest in sorted
     (lexicographic) order, left-associated, optionally `/ D` — evaluated with the same
     float64 operations in the same order (executor.py:81-106) on the exact box kernel
-    (radius 1..2 in 3-D, 1..4 in 2-D)."""
+    (radius 1..4)."""
     params = params if params is not None else dict(bmap.grid_args)
     divisor, terms, src, dst = _exact_sum(bmap, params)
     offs = [o for _, o in terms]

@@ -367,13 +367,12 @@ def test_exact_box_kernel_order_bitwise(case):
 
 
 def test_exact_box_routes():
-    """The full cube in corpus order goes to XBOX up to radius 2 (the full square up to radius 4
-    in 2-D; 2-D stars to XSTAR); larger boxes, a reordered or incomplete cube go to the
-    bytecode kernel."""
+    """The full cube (square in 2-D) in corpus order goes to XBOX (2-D stars to XSTAR); a
+    reordered or incomplete cube goes to the bytecode kernel."""
     import dataclasses
 
-    for name, kind in (("box3d1r", "xbox"), ("box3d2r", "xbox"), ("j3d27pt", "xbox"), ("box3d3r", "expr"),
-                       ("box3d4r", "expr"), ("box2d4r", "xbox"), ("j2d9pt_gol", "xbox"), ("star2d4r", "xstar"),
+    for name, kind in (("box3d1r", "xbox"), ("box3d2r", "xbox"), ("j3d27pt", "xbox"), ("box3d3r", "xbox"),
+                       ("box3d4r", "xbox"), ("box2d4r", "xbox"), ("j2d9pt_gol", "xbox"), ("star2d4r", "xstar"),
                        ("j2d5pt", "xstar")):
         bound, _ = corpus.config_target(name, (12, 12, 12) if "3d" in name else (12, 12), 1)
         assert match_map(next(_maps(bound.stmts)), exact=True).kind == kind, name

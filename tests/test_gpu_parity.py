@@ -116,9 +116,9 @@ def test_fast_box_kernels_vs_c_oracle(shape, dtype, kernel):
 
 
 @pytest.mark.parametrize("shape,dtype", [((37, 45, 133), "f32"), ((64, 64, 64), "f32"), ((21, 38, 70), "f64")])
-@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r"])
+@pytest.mark.parametrize("kernel", ["j3d27pt", "box3d1r", "box3d2r", "box3d3r", "box3d4r"])
 def test_exact_box_kernels_bitwise_vs_c_oracle(shape, dtype, kernel):
-    """precision='exact' runs the corpus boxes (R <= 2) on the exact box streaming kernel:
+    """precision='exact' runs the corpus boxes (R = 1..4) on the exact box streaming kernel:
     bit-identical to the reference's evaluation (the C oracle, -ffp-contract=off)."""
     from paper_2309_04671_b200.matcher import match_map
 

@@ -15,6 +15,7 @@ import pytest
 from conftest import ROOT, build_case, golden_cases, load_golden
 from paper_2309_04671_b200 import _lib as L
 from paper_2309_04671_b200 import corpus
+from paper_2309_04671_b200.front import node_kind
 from paper_2309_04671_b200.matcher import coef_index, compile_expr, map_box, match_map
 from paper_2309_04671_b200 import PlanError, plan_gpu
 
@@ -385,3 +386,35 @@ def test_exact_box_routes():
     assert p.kind == "expr" and "full box in corpus order" in p.reason
     short = dataclasses.replace(m.kernel, updates=(dataclasses.replace(m.kernel.updates[0], expr=e.left),))
     assert match_map(dataclasses.replace(m, kernel=short), exact=True).kind == "expr"
+
+
+@pytest.mark.parametrize("name,shape", [("box3d1r", (8, 8, 8)), ("box3d4r", (10, 10, 10)), ("box2d4r", (16, 16)),
+                                        ("j2d9pt_gol", (12, 12)), ("star2d4r", (12, 12))])
+def test_exact_descriptors(name, shape):
+    """The C-ABI descriptor of an exact box / 2-D map: kind, radius and the coefficient table in
+    the header's layout (box_coef for <= 125 values, box_coef_ext beyond; 2-D stars use the
+    STAR slots of the grid's own two axes), the divisor passed through."""
+    from paper_2309_04671_b200 import _lib as L
+    from paper_2309_04671_b200.backend import map_desc_for
+
+    bound, _ = corpus.config_target(name, shape, 1)
+    m = next(_maps(bound.stmts))
+    plan = match_map(m, exact=True)
+    d = map_desc_for(plan, {"u": 0, "v": 1}, 0)
+    r = plan.radius
+    if plan.kind == "xbox":
+        assert d.kind == L.STKB_MAP_XBOX and d.radius == r
+        n = (2 * r + 1) ** len(shape)
+        assert len(plan.coef) == n
+        got = [d.box_coef_ext[i] for i in range(n)] if n > 125 else [d.box_coef[i] for i in range(n)]
+        assert got == plan.coef and all(c != 0.0 for c in got)  # every corpus tap is non-zero
+        centre = plan.coef[n // 2]
+        text = m.kernel.updates[0].expr
+        while node_kind(text) == "Binary" and text.op in "+/":
+            text = text.left
+        assert centre == float(text.left.value)  # the first term is the centre's
+    else:
+        assert d.kind == L.STKB_MAP_XSTAR and d.radius == r
+        assert [d.coef[i] for i in range(4 * r + 1)] == plan.coef[:4 * r + 1]  # axes 0, 1 of the 2-D grid
+        assert all(c == 0.0 for c in plan.coef[4 * r + 1:])
+    assert d.divisor == plan.divisor

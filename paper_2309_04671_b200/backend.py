@@ -357,6 +357,13 @@ def run_gpu(unit, plan, grids: dict, bindings: Optional[dict] = None, target: Op
     returns the device-resident grids in page-locked host memory (exact-size
     blocks from a caching pool, ``hostmem.py``; they return to it when freed).
     """
+    try:
+        return _run_gpu(unit, plan, grids, bindings, target, args, scheme, device, precision, pinned)
+    except L.StkbError as e:  # device failures (out of memory, launch errors) are execution errors
+        raise ExecutionError(str(e)) from e
+
+
+def _run_gpu(unit, plan, grids, bindings, target, args, scheme, device, precision, pinned) -> dict:
     bound = _prepare(unit, target, args, scheme)
     check_plan(plan, bound)
     used = []

@@ -62,6 +62,9 @@ thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
+    // a failed runtime call (e.g. cudaMalloc out of memory) also sets the thread's last error;
+    // it is reported here, so clear it (non-sticky errors) lest a later launch check see it
+    if (code == STKB_ERR_CUDA) (void)cudaGetLastError();
     return code;
 }
 

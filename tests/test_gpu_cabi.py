@@ -65,3 +65,25 @@ def test_bad_map_is_reported_not_run():
         assert b"same grid" in lib.stkb_last_error()
     finally:
         lib.stkb_domain_destroy(dom)
+
+
+def test_device_out_of_memory_is_an_execution_error():
+    """A target larger than the GPU's memory fails as the reference's ExecutionError (the CLI's
+    exit 1), not a crash; the device stays usable.  Host grids are lazily allocated zeros."""
+    from paper_2309_04671_b200 import GridBuffer, corpus, plan_gpu, run_gpu
+    from paper_2309_04671_b200.backend import ExecutionError, release_device_cache
+
+    release_device_cache()
+    bound, decls = corpus.config_target("star3d1r", (2048, 2048, 3000), 2, "f64")  # 2 x 101 GB
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    bmap = next(s for s in bound.stmts[0].body if type(s).__name__ == "BoundMap")
+    plan = plan_gpu(bmap.info, {"template": "unroll", "computeCapability": "10.0"})
+    with pytest.raises(ExecutionError, match="out of memory"):
+        run_gpu(bound, plan, grids)
+    del grids
+    small, sdecls = corpus.config_target("star3d1r", (16, 16, 16), 2, "f32")
+    g2 = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in sdecls.items()}
+    g2["u"].interior[...] = 1.0
+    out = run_gpu(small, plan_gpu(next(s for s in small.stmts[0].body if type(s).__name__ == "BoundMap").info,
+                                  {"template": "unroll"}), g2)
+    assert np.isfinite(out["u"].data).all()

@@ -37,6 +37,19 @@ def test_header_and_binding_agree():
     assert header_symbols() == sorted(L.EXPORTS)
 
 
+@pytest.mark.parametrize("cc,std,lang", [("gcc", "-std=c99", "c"), ("g++", "-std=c++11", "c++")])
+def test_header_is_plain_c(cc, std, lang):
+    """include/stkb200.h is a plain C header (extern "C" for C++): it compiles on its own."""
+    import shutil
+    import subprocess
+
+    if shutil.which(cc) is None:
+        pytest.skip(f"needs {cc}")
+    r = subprocess.run([cc, std, "-Wall", "-Wextra", "-Werror", "-fsyntax-only", "-x", lang,
+                        str(ROOT / "include" / "stkb200.h")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
 def test_library_loads_and_exports_every_symbol():
     if not L.LIB_PATH.exists():
         pytest.skip("libstkb200.so not built (run __graft_entry__.build())")

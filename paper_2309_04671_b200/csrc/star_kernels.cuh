@@ -288,8 +288,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
                 // order, so CTAs working at the same time stream neighbouring tiles and
                 // share their halo rows through L2
-                while (true) {
-                    const int item = atomicAdd(a.work_counter + step, 1);
+                // (multi-step launches: every CTA is resident and has about one item per step,
+                // so items are assigned statically: no scheduler atomic after the grid barrier)
+                for (int k = 0;; ++k) {
+                    const int item = nsteps > 1 ? int(blockIdx.x) + k * int(gridDim.x)
+                                                : atomicAdd(a.work_counter + step, 1);
                     if (item >= a.n_items) break;
                     int tx, ty, tz;
                     decode_item(a, item, tx, ty, tz);

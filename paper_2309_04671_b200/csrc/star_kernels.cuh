@@ -288,11 +288,13 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                 // dynamic tile scheduler: items are handed out in (z-chunk, y-tile, x-tile)
                 // order, so CTAs working at the same time stream neighbouring tiles and
                 // share their halo rows through L2
-                // (multi-step launches: every CTA is resident and has about one item per step,
-                // so items are assigned statically: no scheduler atomic after the grid barrier)
+                // (multi-step launches — every CTA is resident and has about one item per step —
+                // and launches with at most one item per CTA assign items statically: no
+                // scheduler atomic after a grid barrier or at the kernel start)
+                const bool fixed = nsteps > 1 || a.n_items <= int(gridDim.x);
                 for (int k = 0;; ++k) {
-                    const int item = nsteps > 1 ? int(blockIdx.x) + k * int(gridDim.x)
-                                                : atomicAdd(a.work_counter + step, 1);
+                    const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x)
+                                           : atomicAdd(a.work_counter + step, 1);
                     if (item >= a.n_items) break;
                     int tx, ty, tz;
                     decode_item(a, item, tx, ty, tz);

@@ -419,17 +419,26 @@ def run_ours(args) -> None:
         pin_out = in_bytes + out_bytes < 0.7 * host_ram_bytes()
         run_gpu(bound, plan, grids, device=local, pinned=pin_out)  # warm: context, kernels, graphs
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        out = run_gpu(bound, plan, grids, device=local, pinned=pin_out)
-        e_sec = time.perf_counter() - t0
+        # timed calls: one, or for short calls (small configurations) the median of up to 9
+        # calls within ~1 s — each call moves its inputs and outputs and runs all K steps
+        secs = []
+        while True:
+            t0 = time.perf_counter()
+            out = run_gpu(bound, plan, grids, device=local, pinned=pin_out)
+            secs.append(time.perf_counter() - t0)
+            if sum(secs) > 1.0 or len(secs) >= 9:
+                break
+            del out
+        e_sec = sorted(secs)[len(secs) // 2]
         from paper_2309_04671_b200.backend import LAST_RUN
 
         e2e = {"value": npts * K / e_sec / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": LAST_RUN["h2d_bytes"] / K, "d2h_bytes_per_step": LAST_RUN["d2h_bytes"] / K,
                "h2d_bytes_per_call": LAST_RUN["h2d_bytes"], "d2h_bytes_per_call": LAST_RUN["d2h_bytes"],
                "gpu_launches": LAST_RUN["launches"], "steps_per_call": K, "seconds": e_sec,
+               "calls_timed": len(secs),
                "reused_domain": LAST_RUN.get("reused_domain"), "pinned_outputs": pin_out,
-               "what": "one run_gpu(bound, plan, grids) call: H2D of the live input grids from pinned host "
+               "what": "one run_gpu(bound, plan, grids) call (the median of `calls_timed` calls): H2D of the live input grids from pinned host "
                        f"memory (a zero-halo grid fully overwritten before any read needs no copy), {K} time "
                        "steps (CUDA graph), D2H of every grid; wall clock; bytes per step = bytes per call / "
                        "steps (a time-stepping call moves its grids once)"}

@@ -99,8 +99,10 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
             const CUtensorMap* own = interior ? &tm_int : &tm_src;
             prefetch_tmap(own);
             uint32_t it = 0;
-            while (true) {
-                const int item = atomicAdd(a.work_counter, 1);
+            // at most one item per CTA: static assignment, no scheduler atomic (star_kernels.cuh)
+            const bool fixed = a.n_items <= int(gridDim.x);
+            for (int k = 0;; ++k) {
+                const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
                 if (item >= a.n_items) break;
                 int tx, ty, tz;
                 decode_item(a, item, tx, ty, tz);

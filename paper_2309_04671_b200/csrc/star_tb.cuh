@@ -120,8 +120,10 @@ star_tb2_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constan
             // v's frozen values around the box are all zero (the usual zero halo): no v tiles
             const bool need_v = *reinterpret_cast<const volatile int32_t*>(frozen_nz) != 0;
             uint32_t it = 0;
-            while (true) {
-                const int item = atomicAdd(a.work_counter, 1);
+            // at most one item per CTA: static assignment, no scheduler atomic (star_kernels.cuh)
+            const bool fixed = a.n_items <= int(gridDim.x);
+            for (int k = 0;; ++k) {
+                const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
                 if (item >= a.n_items) {
                     const uint32_t s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);

@@ -80,6 +80,7 @@ __device__ __forceinline__ void xdiv(const double (&a)[N], double d, double y, d
 template <typename T, int R, bool DIV, bool D0 = true>
 __global__ void __launch_bounds__((XstarCfg<T, R>::NWY + 1) * 32, 1)
 star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
+                  const __grid_constant__ CUtensorMap tm_alt, const __grid_constant__ CUtensorMap tm_alt_int,
                   const __grid_constant__ StarArgs<T> a, const __grid_constant__ XstarCoef xc) {
     constexpr int RZ = D0 ? R : 0;  // d0 radius
     using C = XstarCfg<T, R>;
@@ -109,37 +110,54 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
     if (warp == NWY) {
         // ------------------------------------------------------------ producer (star_kernels.cuh)
         if (lane == 0) {
-            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
-            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
-                      iz = interior ? int(a.g.order0) : 0;
-            const CUtensorMap* own = interior ? &tm_int : &tm_src;
-            prefetch_tmap(own);
+            // multi-step launches (small grids, star_kernels.cuh): odd steps read the dst buffer
+            // through the alternate maps; a grid barrier separates the steps
+            const int nsteps = D0 ? a.n_steps : 1;
+            const bool int0 = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            const bool int1 = nsteps > 1 && a.halo_nz_alt && *reinterpret_cast<const volatile int32_t*>(a.halo_nz_alt) == 0;
             uint32_t it = 0;
-            // at most one item per CTA: static assignment, no scheduler atomic (star_kernels.cuh)
-            const bool fixed = a.n_items <= int(gridDim.x);
-            for (int k = 0;; ++k) {
-                const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
-                if (item >= a.n_items) break;
-                int tx, ty, tz;
-                decode_item(a, item, tx, ty, tz);
-                const int x0 = a.x0base + tx * BX;
-                const int y0 = a.box.lo1 + ty * BY;
-                const int z0 = a.zs[2 * tz];
-                const int z1 = a.zs[2 * tz + 1];
-                const int c0 = int(a.g.lead) + x0 - RA - ix;
-                const int c1 = y0 + int(a.g.order) - R - iy;
-                for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
-                    const uint32_t s = it % STAGES;
-                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
-                    stage_item[s] = item;
-                    mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
-                    tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+            // at most one item per CTA (always in multi-step launches): static assignment
+            const bool fixed = nsteps > 1 || a.n_items <= int(gridDim.x);
+            for (int step = 0; step < nsteps; ++step) {
+                const bool odd = (step & 1) != 0;
+                const bool interior = odd ? int1 : int0;
+                const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                          iz = interior ? int(a.g.order0) : 0;
+                const CUtensorMap* own = odd ? (interior ? &tm_alt_int : &tm_alt) : (interior ? &tm_int : &tm_src);
+                if (step == 0) prefetch_tmap(own);
+                if (step > 0) {
+                    const int32_t target = int32_t(gridDim.x) * step;
+                    while (ld_acquire_gpu(a.step_arrive) < target) {
+                    }
+                    fence_proxy_async_global();
                 }
+                for (int k = 0;; ++k) {
+                    const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
+                    if (item >= a.n_items) break;
+                    int tx, ty, tz;
+                    decode_item(a, item, tx, ty, tz);
+                    const int x0 = a.x0base + tx * BX;
+                    const int y0 = a.box.lo1 + ty * BY;
+                    const int z0 = a.zs[2 * tz];
+                    const int z1 = a.zs[2 * tz + 1];
+                    const int c0 = int(a.g.lead) + x0 - RA - ix;
+                    const int c1 = y0 + int(a.g.order) - R - iy;
+                    const int tag = item + step * a.n_items;  // the consumers recover the step
+                    for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
+                        const uint32_t s = it % STAGES;
+                        mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                        stage_item[s] = tag;
+                        mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
+                        tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+                    }
+                }
+                // end of a step (-2) or of the launch (-1): a stage without data
+                const uint32_t s = it % STAGES;
+                mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                stage_item[s] = step + 1 < nsteps ? -2 : -1;
+                mbar_arrive(&full[s]);
+                ++it;
             }
-            const uint32_t s = it % STAGES;
-            mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
-            stage_item[s] = -1;
-            mbar_arrive(&full[s]);
         }
         return;
     }
@@ -231,8 +249,24 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
-        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
-        if (item < 0) break;
+        const int tag = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
+        if (tag == -1) break;
+        if (tag == -2) {
+            // multi-step launch: this CTA's outputs of the step are stored; publish them
+            // (star_kernels.cuh: one gpu-scope fence per CTA after the consumer barrier)
+            fence_proxy_async_global();
+            asm volatile("bar.sync 1, %0;" ::"r"(NWY * 32) : "memory");
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(a.step_arrive, 1);
+            }
+            __syncwarp();
+            mbar_arrive_lane0(&empty[it % STAGES], lane);
+            ++it;
+            continue;
+        }
+        const int step = a.n_steps > 1 ? tag / a.n_items : 0;
+        const int item = tag - step * a.n_items;
         int tx, ty, tz;
         decode_item(a, item, tx, ty, tz);
         const int x0 = a.x0base + tx * BX;
@@ -245,7 +279,7 @@ star_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_const
         const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
         const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
         const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
-        T* const dst0 = a.dst + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+        T* const dst0 = ((step & 1) ? a.dst_alt : a.dst) + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
 
         // plane qi = q - (z0 - R) lives in ring slot qi mod R: unrolled by R, slots are static
         for (int qb = 0; qb < nq; qb += R) {
@@ -614,10 +648,19 @@ cudaError_t launch_exact_cfg(const StarLaunch& L, StarArgs<T> a, const XstarCoef
     const int n0 = a.box.hi0 - a.box.lo0;
     const int tiles = a.n_tx * a.n_ty;
     const int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
+    const bool multi = D0 && L.n_steps > 1;
     int ntz;
-    a.lz = L.lz > 0 ? L.lz : choose_lz(n0, tiles, ctas, R, &ntz);
-    if (L.lz <= 0 && ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
-    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper, a.zs, 0);
+    if (L.lz > 0) {
+        a.lz = L.lz;
+    } else if (multi && tiles < ctas) {
+        // one item per CTA and step, the shortest chunks that fit one wave (star_kernels.cuh)
+        const int per_tile = std::max(1, ctas / tiles);
+        a.lz = (n0 + per_tile - 1) / per_tile;
+    } else {
+        a.lz = choose_lz(n0, tiles, ctas, R, &ntz);
+        if (ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
+    }
+    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper && !multi, a.zs, 0);
     a.n_signal = 0;
     a.band_rows = 0;
     if (L.band_pct > 0 && a.n_tx > 0) {
@@ -625,12 +668,30 @@ cudaError_t launch_exact_cfg(const StarLaunch& L, StarArgs<T> a, const XstarCoef
         if (rows < a.n_ty) a.band_rows = rows;
     }
     a.n_items = tiles * a.n_tz;
-    a.n_steps = 1;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;
+    if (multi) {
+        // several steps, a grid barrier between them: a cooperative launch (every CTA resident)
+        a.n_steps = L.n_steps;
+        a.step_arrive = L.step_counters + L.n_steps;
+        cudaError_t e = cudaMemsetAsync(L.step_counters, 0, (L.n_steps + 1) * sizeof(int32_t), stream);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[6], maps[4], maps[5], a, xc);
+    }
+    a.n_steps = 1;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], a, xc);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], maps[0], maps[6], a, xc);
     return cudaGetLastError();
 }
 

@@ -499,7 +499,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         if constexpr (sizeof(T) == 4) e = launch_xbox_f32(L, a, xc, dom->stream);
         else e = launch_xbox_f64(L, a, xc, dom->stream);
     } else if (d.kind == STKB_MAP_XSTAR) {
-        if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
+        if (rs.n > 0 || pull || (n_steps > 1 && exact2d))
+            return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
         XstarCoef xc{};
         xc.c0 = d.coef[0];
         // a 2-D star's axes (d0, d1 of the grid) are the lifted plane's d1, d2
@@ -620,7 +621,8 @@ const MapOp* multi_map(const stkb_domain* dom) {
     if (m.kind != 0 || w.kind != 1) return nullptr;
     const MapOp& op = dom->maps[m.map];
     const stkb_map_desc& d = op.d;
-    if (d.kind != STKB_MAP_STAR || d.precision != STKB_PREC_FAST) return nullptr;
+    // fast stars and the exact star (the same streaming structure and multi-step protocol)
+    if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_XSTAR) || d.precision != STKB_PREC_FAST) return nullptr;
     if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;
     if (d.lo[0] >= d.hi[0] || d.lo[1] >= d.hi[1] || d.lo[2] >= d.hi[2]) return nullptr;
     return &op;

@@ -148,3 +148,24 @@ def test_small_grid_tile_bitwise_equal_default_tile(monkeypatch, builder, dtype,
             outs.append({n: dt.download(n) for n in names})
     for n in names:
         assert np.array_equal(outs[0][n], outs[1][n]), n
+
+
+@pytest.mark.parametrize("builder,dtype,shape,steps", [("star3d4r", "f32", (128, 128, 128), 10),
+                                                       ("star3d4r_norm", "f32", (37, 45, 133), 7),
+                                                       ("jacobi7", "f32", (64, 72, 96), 12),
+                                                       ("star3d2r_norm", "f64", (48, 40, 64), 5),
+                                                       ("star3d1r", "f32", (9, 20, 40), 70)])
+def test_exact_multi_step_bitwise_vs_oracle(builder, dtype, shape, steps):
+    """precision='exact' small-grid ping-pongs run their steps in multi-step launches of the
+    exact star kernel (one launch per 64 steps): bit for bit the reference's evaluation."""
+    from paper_2309_04671_b200.backend import LAST_RUN
+
+    bound, decls = corpus.config_target(builder, shape, steps, dtype)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    fill_loguniform(grids["u"], 11)
+    plan = plan_gpu(bound.stmts[0].body[0].info, {"template": "unroll", "computeCapability": "10.0"})
+    got = run_gpu(bound, plan, grids, precision="exact")
+    assert LAST_RUN["launches"] == math.ceil(steps / 64)
+    ref = oracle.run_target_c(bound, grids)
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), (builder, n, compare(ref[n], got[n]).render())

@@ -58,7 +58,8 @@ def _run(bound, grids, steps, multi, box=None, runs=(None,)):
 
 
 @pytest.mark.parametrize("builder,dtype", [("star3d4r", "f32"), ("star3d4r_norm", "f32"), ("star3d1r", "f32"),
-                                           ("star3d2r", "f64"), ("star3d3r", "f32"), ("star3d4r_norm", "f64")])
+                                           ("star3d2r", "f64"), ("star3d3r", "f32"), ("star3d4r_norm", "f64"),
+                                           ("j3d27pt", "f32"), ("box3d2r", "f64")])
 @pytest.mark.parametrize("shape", [(37, 45, 133), (128, 128, 128), (9, 20, 40)])
 @pytest.mark.parametrize("steps", [2, 3, 10])
 def test_multi_step_bitwise_equal_single_steps(builder, dtype, shape, steps):
@@ -95,7 +96,8 @@ def test_multi_step_sub_box_and_halo(box, halo):
 
 @pytest.mark.parametrize("builder,dtype,shape,steps", [("star3d4r", "f32", (128, 128, 128), 10),
                                                        ("jacobi7", "f32", (64, 72, 96), 12),
-                                                       ("star3d2r_norm", "f64", (48, 40, 64), 7)])
+                                                       ("star3d2r_norm", "f64", (48, 40, 64), 7),
+                                                       ("j3d27pt", "f32", (64, 48, 80), 9)])
 def test_multi_step_run_gpu_vs_oracle(builder, dtype, shape, steps):
     """The public path (run_gpu) on BASELINE config c1's program and shape: one launch for
     all steps, within the fast-path tolerance of the reference oracle."""

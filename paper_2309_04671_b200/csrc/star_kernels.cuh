@@ -343,8 +343,11 @@ star_stream_kernel(const __grid_constant__ CUtensorMap tm_src,
                                 const int cx = int(a.g.lead) + x0;
                                 const int cy = y0 + int(a.g.order);
                                 const int cz = z + int(a.g.order0);
-                                tma_load_3d(st + C::HALO_ELEMS, &tm_ctr, &full[s], cx, cy, cz);
-                                tma_load_3d(st + C::HALO_ELEMS + C::CTR_ELEMS, &tm_prev, &full[s], cx, cy, cz);
+                                // multi-step (in-place wave ping-pong: prev is dst): odd steps
+                                // read u from the dst buffer and u_prev from the src buffer
+                                tma_load_3d(st + C::HALO_ELEMS, odd ? &tm_prev : &tm_ctr, &full[s], cx, cy, cz);
+                                tma_load_3d(st + C::HALO_ELEMS + C::CTR_ELEMS, odd ? &tm_ctr : &tm_prev, &full[s], cx,
+                                            cy, cz);
                                 tma_load_3d(st + C::HALO_ELEMS + 2 * C::CTR_ELEMS, &tm_vel, &full[s], cx, cy, cz);
                             }
                         } else {

@@ -621,8 +621,11 @@ const MapOp* multi_map(const stkb_domain* dom) {
     if (m.kind != 0 || w.kind != 1) return nullptr;
     const MapOp& op = dom->maps[m.map];
     const stkb_map_desc& d = op.d;
-    // fast stars and boxes and the exact star (the same streaming structure and multi-step protocol)
-    if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR) || d.precision != STKB_PREC_FAST)
+    // fast stars, boxes and the in-place wave, and the exact star (the same streaming structure
+    // and multi-step protocol; the wave's odd steps swap its u / u_prev centre maps)
+    const bool wave_ok = d.kind == STKB_MAP_WAVE && d.prev == d.dst;
+    if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR && !wave_ok) ||
+        d.precision != STKB_PREC_FAST)
         return nullptr;
     if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;
     if (d.lo[0] >= d.hi[0] || d.lo[1] >= d.hi[1] || d.lo[2] >= d.hi[2]) return nullptr;

@@ -99,6 +99,21 @@ struct XstarCoef {
     double recip;     // RN(1 / divisor) when the divisor is in [2^-64, 2^64] (xdiv), else 0
 };
 
+// arguments of the 1.5-D kernel for 2-D grids (star2d.cu)
+struct Star2DArgs {
+    int64_t pitch;   // elements between consecutive d0 rows
+    int64_t lead;    // column of interior d1 = 0
+    int32_t order;   // halo (rows and columns)
+    int32_t lo0, hi0, lo1, hi1;  // output box (interior coordinates)
+    int32_t x0base;  // lo1 rounded down to the vector width
+    int32_t n_tx, lz, n_tz;
+    int32_t* nonfinite;
+    double c0, cm0[4], cp0[4], cm1[4], cp1[4];  // d0 / d1 coefficients (offset -m / +m)
+    double rdiv;     // 1/divisor or 0
+    int32_t box;     // dense (2R+1)^2 coefficient square instead of the star
+    double cb[81];   // box: cb[(dy+R)*(2R+1) + (dx+R)]
+};
+
 // coefficients of the exact box kernel (box_exact.cu): c[((dz+R)(2R+1) + (dy+R))(2R+1) + (dx+R)]
 struct XboxCoef {
     double c[729];  // 3-D radius <= 4; 2-D: c[(dy+R)(2R+1) + (dx+R)], radius <= 4

@@ -14,19 +14,7 @@
 
 namespace stkb {
 
-struct Star2DArgs {
-    int64_t pitch;   // elements between consecutive d0 rows
-    int64_t lead;    // column of interior d1 = 0
-    int32_t order;   // halo (rows and columns)
-    int32_t lo0, hi0, lo1, hi1;  // output box (interior coordinates)
-    int32_t x0base;  // lo1 rounded down to the vector width
-    int32_t n_tx, lz, n_tz;
-    int32_t* nonfinite;
-    double c0, cm0[4], cp0[4], cm1[4], cp1[4];  // d0 / d1 coefficients (offset -m / +m)
-    double rdiv;     // 1/divisor or 0
-    int32_t box;     // dense (2R+1)^2 coefficient square instead of the star
-    double cb[81];   // box: cb[(dy+R)*(2R+1) + (dx+R)]
-};
+// Star2DArgs: common.cuh (shared with the host side of stkb200.cu)
 
 // the same coefficients in the grid dtype, read straight from the parameter bank
 template <typename T>

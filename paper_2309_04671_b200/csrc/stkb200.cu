@@ -31,19 +31,7 @@ cudaError_t launch_signal_add(int32_t* p, int32_t v, cudaStream_t s);
 cudaError_t launch_repitch(void* stage, void* dev, int64_t r0, int64_t nrows, int64_t rows_per_plane,
                            int64_t row_bytes, int64_t row_pitch_bytes, int64_t plane_pitch_bytes, bool to_device,
                            int num_sms, cudaStream_t s);
-struct Star2DArgs {
-    int64_t pitch;
-    int64_t lead;
-    int32_t order;
-    int32_t lo0, hi0, lo1, hi1;
-    int32_t x0base;
-    int32_t n_tx, lz, n_tz;
-    int32_t* nonfinite;
-    double c0, cm0[4], cp0[4], cm1[4], cp1[4];
-    double rdiv;
-    int32_t box;
-    double cb[81];
-};
+// Star2DArgs: common.cuh
 cudaError_t launch_tb2_f32(const StarLaunch& L, const StarArgs<float>& a, cudaStream_t s);
 cudaError_t launch_tb2_f64(const StarLaunch& L, const StarArgs<double>& a, cudaStream_t s);
 int tb2_tile(int dtype, int radius, int* box_w, int* box_h, int* v_w, int* v_h);

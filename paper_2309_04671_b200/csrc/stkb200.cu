@@ -470,7 +470,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
     }
     cudaError_t e;
     if (d.kind == STKB_MAP_XWAVE) {
-        if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact wave maps launch over their box");
+        if (rs.n > 0 || pull || (n_steps > 1 && d.prev != d.dst))
+            return fail(STKB_ERR_UNSUPPORTED, "exact wave maps launch over their box");
         XwaveCoef xc{};
         xc.a = d.wave_a;
         xc.c0 = d.coef[0];
@@ -611,7 +612,7 @@ const MapOp* multi_map(const stkb_domain* dom) {
     const stkb_map_desc& d = op.d;
     // fast stars, boxes and the in-place wave, and the exact star (the same streaming structure
     // and multi-step protocol; the wave's odd steps swap its u / u_prev centre maps)
-    const bool wave_ok = d.kind == STKB_MAP_WAVE && d.prev == d.dst;
+    const bool wave_ok = (d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_XWAVE) && d.prev == d.dst;
     if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR && !wave_ok) ||
         d.precision != STKB_PREC_FAST)
         return nullptr;

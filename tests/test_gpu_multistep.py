@@ -203,3 +203,21 @@ def test_wave_multi_step_bitwise_equal_single_steps(shape, dtype, steps):
     for n in ref:
         got = GridBuffer(ref[n].dtype, ref[n].shape, ref[n].order, outs[1][n])
         assert compare(ref[n], got).max_relative <= TOL[dtype], n
+
+
+@pytest.mark.parametrize("shape,dtype,steps", [((40, 48, 136), "f32", 6), ((64, 64, 64), "f32", 70),
+                                               ((33, 20, 70), "f64", 5)])
+def test_exact_wave_multi_step_bitwise_vs_oracle(shape, dtype, steps):
+    """precision='exact' small-grid acoustic waves run their steps in multi-step launches of the
+    exact wave kernel: bit for bit the reference's evaluation."""
+    from paper_2309_04671_b200.backend import LAST_RUN
+
+    bound, decls = corpus.wave_target(shape, steps, dtype)
+    grids = {n: GridBuffer.zeros(d.shape, d.order, d.dtype) for n, d in decls.items()}
+    corpus.wave_inputs(grids)
+    plan = plan_gpu(bound.stmts[0].body[0].info, {"template": "unroll", "computeCapability": "10.0"})
+    got = run_gpu(bound, plan, grids, precision="exact")
+    assert LAST_RUN["launches"] == math.ceil(steps / 64)
+    ref = oracle.run_target_c(bound, grids)
+    for n in ref:
+        assert np.array_equal(ref[n].data, got[n].data), (n, compare(ref[n], got[n]).render())

@@ -64,6 +64,7 @@ __device__ __forceinline__ void xbox_row(const T* row, double* xr) {
 template <typename T, int R, bool DIV, bool D0 = true>
 __global__ void __launch_bounds__((XboxCfg<T, R, D0>::NWY + 1) * 32, 1)
 box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_int,
+                 const __grid_constant__ CUtensorMap tm_alt, const __grid_constant__ CUtensorMap tm_alt_int,
                  const __grid_constant__ StarArgs<T> a, const __grid_constant__ XboxCoef xc) {
     using C = XboxCfg<T, R, D0>;
     constexpr int RZ = D0 ? R : 0;  // d0 radius
@@ -93,37 +94,51 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
     if (warp == NWY) {
         // ------------------------------------------------------------ producer (star_kernels.cuh)
         if (lane == 0) {
-            const bool interior = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
-            const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
-                      iz = interior ? int(a.g.order0) : 0;
-            const CUtensorMap* own = interior ? &tm_int : &tm_src;
-            prefetch_tmap(own);
+            // multi-step launches (small 3-D grids): as star_exact_kernel
+            const int nsteps = D0 && a.n_steps > 1 ? a.n_steps : 1;
+            const bool int0 = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
+            const bool int1 = nsteps > 1 && a.halo_nz_alt && *reinterpret_cast<const volatile int32_t*>(a.halo_nz_alt) == 0;
             uint32_t it = 0;
-            // at most one item per CTA: static assignment, no scheduler atomic (star_kernels.cuh)
-            const bool fixed = a.n_items <= int(gridDim.x);
-            for (int k = 0;; ++k) {
-                const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
-                if (item >= a.n_items) break;
-                int tx, ty, tz;
-                decode_item(a, item, tx, ty, tz);
-                const int x0 = a.x0base + tx * BX;
-                const int y0 = a.box.lo1 + ty * BY;
-                const int z0 = a.zs[2 * tz];
-                const int z1 = a.zs[2 * tz + 1];
-                const int c0 = int(a.g.lead) + x0 - RA - ix;
-                const int c1 = y0 + int(a.g.order) - R - iy;
-                for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
-                    const uint32_t s = it % STAGES;
-                    mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
-                    stage_item[s] = item;
-                    mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
-                    tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+            const bool fixed = nsteps > 1 || a.n_items <= int(gridDim.x);
+            for (int step = 0; step < nsteps; ++step) {
+                const bool odd = (step & 1) != 0;
+                const bool interior = odd ? int1 : int0;
+                const int ix = interior ? int(a.g.lead) : 0, iy = interior ? int(a.g.order) : 0,
+                          iz = interior ? int(a.g.order0) : 0;
+                const CUtensorMap* own = odd ? (interior ? &tm_alt_int : &tm_alt) : (interior ? &tm_int : &tm_src);
+                if (step == 0) prefetch_tmap(own);
+                if (step > 0) {
+                    const int32_t target = int32_t(gridDim.x) * step;
+                    while (ld_acquire_gpu(a.step_arrive) < target) {
+                    }
+                    fence_proxy_async_global();
                 }
+                for (int k = 0;; ++k) {
+                    const int item = fixed ? int(blockIdx.x) + k * int(gridDim.x) : atomicAdd(a.work_counter, 1);
+                    if (item >= a.n_items) break;
+                    int tx, ty, tz;
+                    decode_item(a, item, tx, ty, tz);
+                    const int x0 = a.x0base + tx * BX;
+                    const int y0 = a.box.lo1 + ty * BY;
+                    const int z0 = a.zs[2 * tz];
+                    const int z1 = a.zs[2 * tz + 1];
+                    const int c0 = int(a.g.lead) + x0 - RA - ix;
+                    const int c1 = y0 + int(a.g.order) - R - iy;
+                    const int tag = item + step * a.n_items;
+                    for (int q = z0 - RZ; q < z1 + RZ; ++q, ++it) {
+                        const uint32_t s = it % STAGES;
+                        mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                        stage_item[s] = tag;
+                        mbar_arrive_expect_tx(&full[s], C::HALO_BYTES);
+                        tma_load_3d(tiles + size_t(s) * C::HALO_ELEMS, own, &full[s], c0, c1, q + int(a.g.order0) - iz);
+                    }
+                }
+                const uint32_t s = it % STAGES;
+                mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+                stage_item[s] = step + 1 < nsteps ? -2 : -1;
+                mbar_arrive(&full[s]);
+                ++it;
             }
-            const uint32_t s = it % STAGES;
-            mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
-            stage_item[s] = -1;
-            mbar_arrive(&full[s]);
         }
         return;
     }
@@ -202,8 +217,22 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
 
     while (true) {
         mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
-        const int item = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
-        if (item < 0) break;
+        const int tag = __shfl_sync(0xffffffffu, stage_item[it % STAGES], 0);
+        if (tag == -1) break;
+        if (tag == -2) {  // multi-step: publish this CTA's outputs of the step (star_exact_kernel)
+            fence_proxy_async_global();
+            asm volatile("bar.sync 1, %0;" ::"r"(NWY * 32) : "memory");
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(a.step_arrive, 1);
+            }
+            __syncwarp();
+            mbar_arrive_lane0(&empty[it % STAGES], lane);
+            ++it;
+            continue;
+        }
+        const int step = a.n_steps > 1 ? tag / a.n_items : 0;
+        const int item = tag - step * a.n_items;
         int tx, ty, tz;
         decode_item(a, item, tx, ty, tz);
         const int x0 = a.x0base + tx * BX;
@@ -216,7 +245,7 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
         const bool y_in = y >= a.box.lo1 && y < a.box.hi1;
         const bool x_full = x >= a.box.lo2 && x + VEC <= a.box.hi2;
         const bool x_any = x + VEC > a.box.lo2 && x < a.box.hi2;
-        T* const dst0 = a.dst + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+        T* const dst0 = ((step & 1) ? a.dst_alt : a.dst) + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
         const uint32_t it0 = it;
 
         // plane qi = q - (z0 - R) lives in ring slot qi mod R: unrolled by R, slots are static
@@ -324,10 +353,18 @@ cudaError_t launch_xbox_cfg(const StarLaunch& L, StarArgs<T> a, const XboxCoef& 
     const int n0 = a.box.hi0 - a.box.lo0;
     const int tiles = a.n_tx * a.n_ty;
     const int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
+    const bool multi = D0 && L.n_steps > 1;
     int ntz;
-    a.lz = L.lz > 0 ? L.lz : choose_lz(n0, tiles, ctas, R, &ntz);
-    if (L.lz <= 0 && ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
-    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper, a.zs, 0);
+    if (L.lz > 0) {
+        a.lz = L.lz;
+    } else if (multi && tiles < ctas) {
+        const int per_tile = std::max(1, ctas / tiles);
+        a.lz = (n0 + per_tile - 1) / per_tile;
+    } else {
+        a.lz = choose_lz(n0, tiles, ctas, R, &ntz);
+        if (ntz > kMaxChunks / 2) a.lz = (n0 + kMaxChunks / 2 - 1) / (kMaxChunks / 2);
+    }
+    a.n_tz = chunk_range(a.box.lo0, n0, a.lz, tiles, ctas, L.taper && !multi, a.zs, 0);
     a.n_signal = 0;
     a.band_rows = 0;
     if (L.band_pct > 0 && a.n_tx > 0) {
@@ -335,12 +372,29 @@ cudaError_t launch_xbox_cfg(const StarLaunch& L, StarArgs<T> a, const XboxCoef& 
         if (rows < a.n_ty) a.band_rows = rows;
     }
     a.n_items = tiles * a.n_tz;
-    a.n_steps = 1;
     if (a.n_items <= 0) return cudaSuccess;
     const int grid = a.n_items < ctas ? a.n_items : ctas;
+    if (multi) {
+        a.n_steps = L.n_steps;
+        a.step_arrive = L.step_counters + L.n_steps;
+        cudaError_t e = cudaMemsetAsync(L.step_counters, 0, (L.n_steps + 1) * sizeof(int32_t), stream);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[6], maps[4], maps[5], a, xc);
+    }
+    a.n_steps = 1;
     cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], a, xc);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(maps[0], maps[6], maps[0], maps[6], a, xc);
     return cudaGetLastError();
 }
 

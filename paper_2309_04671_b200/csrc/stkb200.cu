@@ -479,7 +479,8 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         if constexpr (sizeof(T) == 4) e = launch_xwave_f32(L, a, xc, dom->stream);
         else e = launch_xwave_f64(L, a, xc, dom->stream);
     } else if (d.kind == STKB_MAP_XBOX) {
-        if (rs.n > 0 || pull || n_steps > 1) return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
+        if (rs.n > 0 || pull || (n_steps > 1 && exact2d))
+            return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
         XboxCoef xc{};
         for (size_t i = 0; i < op.cube.size() && i < 729; ++i) xc.c[i] = op.cube[i];
         xc.divisor = d.divisor;
@@ -613,7 +614,8 @@ const MapOp* multi_map(const stkb_domain* dom) {
     // fast stars, boxes and the in-place wave, and the exact star (the same streaming structure
     // and multi-step protocol; the wave's odd steps swap its u / u_prev centre maps)
     const bool wave_ok = (d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_XWAVE) && d.prev == d.dst;
-    if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR && !wave_ok) ||
+    if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR && d.kind != STKB_MAP_XBOX &&
+         !wave_ok) ||
         d.precision != STKB_PREC_FAST)
         return nullptr;
     if (!((w.a == d.src && w.b == d.dst) || (w.a == d.dst && w.b == d.src))) return nullptr;

@@ -156,10 +156,13 @@ def test_small_grid_tile_bitwise_equal_default_tile(monkeypatch, builder, dtype,
                                                        ("star3d4r_norm", "f32", (37, 45, 133), 7),
                                                        ("jacobi7", "f32", (64, 72, 96), 12),
                                                        ("star3d2r_norm", "f64", (48, 40, 64), 5),
-                                                       ("star3d1r", "f32", (9, 20, 40), 70)])
+                                                       ("star3d1r", "f32", (9, 20, 40), 70),
+                                                       ("j3d27pt", "f32", (40, 48, 70), 9),
+                                                       ("box3d2r", "f64", (30, 26, 40), 4),
+                                                       ("box3d4r", "f32", (20, 24, 30), 3)])
 def test_exact_multi_step_bitwise_vs_oracle(builder, dtype, shape, steps):
     """precision='exact' small-grid ping-pongs run their steps in multi-step launches of the
-    exact star kernel (one launch per 64 steps): bit for bit the reference's evaluation."""
+    exact star and box kernels (one launch per 64 steps): bit for bit the reference's evaluation."""
     from paper_2309_04671_b200.backend import LAST_RUN
 
     bound, decls = corpus.config_target(builder, shape, steps, dtype)

@@ -95,7 +95,7 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
         // ------------------------------------------------------------ producer (star_kernels.cuh)
         if (lane == 0) {
             // multi-step launches (small 3-D grids): as star_exact_kernel
-            const int nsteps = D0 && a.n_steps > 1 ? a.n_steps : 1;
+            const int nsteps = a.n_steps > 1 ? a.n_steps : 1;
             const bool int0 = a.halo_nz && *reinterpret_cast<const volatile int32_t*>(a.halo_nz) == 0;
             const bool int1 = nsteps > 1 && a.halo_nz_alt && *reinterpret_cast<const volatile int32_t*>(a.halo_nz_alt) == 0;
             uint32_t it = 0;
@@ -154,8 +154,23 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
         while (true) {
             const uint32_t s = it2 % STAGES;
             mbar_wait(&full[s], (it2 / STAGES) & 1u);
-            const int item = __shfl_sync(0xffffffffu, stage_item[s], 0);
-            if (item < 0) break;
+            const int tag = __shfl_sync(0xffffffffu, stage_item[s], 0);
+            if (tag == -1) break;
+            if (tag == -2) {  // multi-step: publish this CTA's outputs of the step
+                fence_proxy_async_global();
+                asm volatile("bar.sync 1, %0;" ::"r"(NWY * 32) : "memory");
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    atomicAdd(a.step_arrive, 1);
+                }
+                __syncwarp();
+                mbar_arrive_lane0(&empty[s], lane);
+                ++it2;
+                continue;
+            }
+            const int step = a.n_steps > 1 ? tag / a.n_items : 0;
+            const int item = tag - step * a.n_items;
+            T* const dstep = (step & 1) ? a.dst_alt : a.dst;
             int tx, ty, tz;
             decode_item(a, item, tx, ty, tz);
             const int x = a.x0base + tx * BX + xl;
@@ -198,7 +213,7 @@ box_exact_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_consta
                     outv[i] = T(DIV ? qv[i] : acc[i]);
                     chk2 = fma_t(T(0), outv[i], chk2);
                 }
-                T* const dz = a.dst + (int64_t(z) + a.g.order0) * plane + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
+                T* const dz = dstep + (int64_t(z) + a.g.order0) * plane + (int64_t(y) + a.g.order) * pitch + a.g.lead + x;
                 if (y_in && x_full) stg16(dz, outv);
                 else if (y_in && x_any)
                     store_row_masked<T>(dz, outv[0], outv[1 % VEC], outv[2 % VEC], outv[3 % VEC], x, a.box.lo2,
@@ -353,7 +368,7 @@ cudaError_t launch_xbox_cfg(const StarLaunch& L, StarArgs<T> a, const XboxCoef& 
     const int n0 = a.box.hi0 - a.box.lo0;
     const int tiles = a.n_tx * a.n_ty;
     const int ctas = L.max_ctas > 0 ? L.max_ctas : L.num_sms;
-    const bool multi = D0 && L.n_steps > 1;
+    const bool multi = L.n_steps > 1;
     int ntz;
     if (L.lz > 0) {
         a.lz = L.lz;

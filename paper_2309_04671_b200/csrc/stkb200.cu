@@ -427,11 +427,16 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         const int db = bind[d.dst];
         const CUtensorMap *m_alt = nullptr, *m_alt_int = nullptr;
         if ((rc = encode_map(dom, db, lw, lh, &m_alt))) return rc;
-        if ((rc = encode_map_int(dom, db, lw, lh, &m_alt_int))) return rc;
         maps[4] = *m_alt;
-        maps[5] = *m_alt_int;
         a.dst_alt = static_cast<T*>(dom->bufs[sb]);
-        a.halo_nz_alt = dom->halo_external ? nullptr : dom->d_flags + kHaloFlag + db;
+        if (dom->desc.ndim == 3) {
+            if ((rc = encode_map_int(dom, db, lw, lh, &m_alt_int))) return rc;
+            maps[5] = *m_alt_int;
+            a.halo_nz_alt = dom->halo_external ? nullptr : dom->d_flags + kHaloFlag + db;
+        } else {  // 2-D (exact one-plane mode): halo flags are 3-D only; always the full map
+            maps[5] = *m_alt;
+            a.halo_nz_alt = nullptr;
+        }
     }
     if (d.kind == STKB_MAP_WAVE) {
         const CUtensorMap *mc, *mp, *mv;
@@ -479,8 +484,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         if constexpr (sizeof(T) == 4) e = launch_xwave_f32(L, a, xc, dom->stream);
         else e = launch_xwave_f64(L, a, xc, dom->stream);
     } else if (d.kind == STKB_MAP_XBOX) {
-        if (rs.n > 0 || pull || (n_steps > 1 && exact2d))
-            return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
+        if (rs.n > 0 || pull) return fail(STKB_ERR_UNSUPPORTED, "exact box maps launch over their box");
         XboxCoef xc{};
         for (size_t i = 0; i < op.cube.size() && i < 729; ++i) xc.c[i] = op.cube[i];
         xc.divisor = d.divisor;
@@ -489,8 +493,7 @@ int launch_star_map(stkb_domain* dom, const MapOp& op, const std::vector<int32_t
         if constexpr (sizeof(T) == 4) e = launch_xbox_f32(L, a, xc, dom->stream);
         else e = launch_xbox_f64(L, a, xc, dom->stream);
     } else if (d.kind == STKB_MAP_XSTAR) {
-        if (rs.n > 0 || pull || (n_steps > 1 && exact2d))
-            return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
+        if (rs.n > 0 || pull) return fail(STKB_ERR_UNSUPPORTED, "exact star maps launch over their box");
         XstarCoef xc{};
         xc.c0 = d.coef[0];
         // a 2-D star's axes (d0, d1 of the grid) are the lifted plane's d1, d2
@@ -604,7 +607,7 @@ const MapOp* tb_map(const stkb_domain* dom) {
 // barrier inside the kernel (StarArgs::n_steps).  Per point the arithmetic is the
 // single-step kernel's, so every grid ends bit-identical to single steps.
 const MapOp* multi_map(const stkb_domain* dom) {
-    if (!dom->multi || dom->desc.ndim != 3 || dom->prog.size() != 2 || dom->halo_external) return nullptr;
+    if (!dom->multi || dom->desc.ndim == 1 || dom->prog.size() != 2 || dom->halo_external) return nullptr;
     if (dom->g.n0 * dom->g.n1 * dom->g.n2 > dom->multi_max_points) return nullptr;
     const ProgOp& m = dom->prog[0];
     const ProgOp& w = dom->prog[1];
@@ -614,6 +617,8 @@ const MapOp* multi_map(const stkb_domain* dom) {
     // fast stars, boxes and the in-place wave, and the exact star (the same streaming structure
     // and multi-step protocol; the wave's odd steps swap its u / u_prev centre maps)
     const bool wave_ok = (d.kind == STKB_MAP_WAVE || d.kind == STKB_MAP_XWAVE) && d.prev == d.dst;
+    // 2-D grids: the exact kernels' one-plane mode (the fast 2-D kernel keeps single steps)
+    if (dom->desc.ndim == 2 && d.kind != STKB_MAP_XSTAR && d.kind != STKB_MAP_XBOX) return nullptr;
     if ((d.kind != STKB_MAP_STAR && d.kind != STKB_MAP_BOX && d.kind != STKB_MAP_XSTAR && d.kind != STKB_MAP_XBOX &&
          !wave_ok) ||
         d.precision != STKB_PREC_FAST)

@@ -159,7 +159,11 @@ def test_small_grid_tile_bitwise_equal_default_tile(monkeypatch, builder, dtype,
                                                        ("star3d1r", "f32", (9, 20, 40), 70),
                                                        ("j3d27pt", "f32", (40, 48, 70), 9),
                                                        ("box3d2r", "f64", (30, 26, 40), 4),
-                                                       ("box3d4r", "f32", (20, 24, 30), 3)])
+                                                       ("box3d4r", "f32", (20, 24, 30), 3),
+                                                       ("star2d4r", "f32", (1000, 1000), 9),
+                                                       ("star2d1r", "f64", (37, 300), 70),
+                                                       ("box2d2r", "f32", (90, 130), 6),
+                                                       ("j2d9pt_gol", "f32", (64, 200), 5)])
 def test_exact_multi_step_bitwise_vs_oracle(builder, dtype, shape, steps):
     """precision='exact' small-grid ping-pongs run their steps in multi-step launches of the
     exact star and box kernels (one launch per 64 steps): bit for bit the reference's evaluation."""

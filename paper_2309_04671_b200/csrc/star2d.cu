@@ -252,6 +252,9 @@ cudaError_t launch2d_t(Star2DArgs a, int R, const void* src, void* dst, bool div
     int tz = (target + a.n_tx - 1) / a.n_tx;
     int lz = (n0 + tz - 1) / tz;
     if (lz < 2 * R) lz = 2 * R;
+    // mid-size grids: chunks of at least 4R rows (each chunk re-streams 2R rows) while a dozen
+    // warps per SM remain (2048^2 radius 4: +16 %; small grids keep the short chunks)
+    if (lz < 4 * R && int64_t(a.n_tx) * ((n0 + 4 * R - 1) / (4 * R)) >= int64_t(num_sms) * 12) lz = 4 * R;
     if (lz > n0) lz = n0;
     a.lz = lz;
     a.n_tz = (n0 + lz - 1) / lz;
